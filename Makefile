@@ -1,0 +1,26 @@
+# Build every native artefact in-tree (the .so files travel to the GPU box with gpurun).
+NVCC    ?= /usr/local/cuda/bin/nvcc
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+PKG     := paper_2605_20497_b200
+CSRC    := $(PKG)/csrc
+CU_SRCS := $(wildcard $(CSRC)/*.cu)
+CU_HDRS := $(wildcard $(CSRC)/*.cuh) include/hgp.h
+
+.PHONY: all gen oracle cuda clean
+all: gen oracle cuda
+
+gen: hgpgen/libhgpgen.so
+hgpgen/libhgpgen.so: hgpgen/hgpgen.c hgpgen/hgpgen.h
+	gcc -O2 -fPIC -shared -std=c11 -Wall -Wextra -o $@ $< -lm
+
+oracle: oracle/libhgp_ref.so
+oracle/libhgp_ref.so: oracle/hgp_ref.cpp oracle/hgp_ref.h
+	g++ -O2 -fPIC -shared -std=c++17 -Wall -Wextra -o $@ $<
+
+cuda: $(PKG)/libhgp.so
+$(PKG)/libhgp.so: $(CU_SRCS) $(CU_HDRS)
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+	  -Xptxas -warn-spills -Iinclude -shared -o $@ $(CU_SRCS) -lcudart
+
+clean:
+	rm -f hgpgen/libhgpgen.so oracle/libhgp_ref.so $(PKG)/libhgp.so

@@ -1,0 +1,17 @@
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path through the C-ABI)")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+    # The host-side libraries are cheap to (re)build; the CUDA library is built by
+    # __graft_entry__.build() / `make cuda` and is never silently skipped on a GPU box.
+    subprocess.run(["make", "-s", "-C", ROOT, "gen", "oracle"], check=True)
