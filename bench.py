@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""bench.py — throughput of one coarsening level of arXiv 2605.20497 on B200.
+
+Metric (BASELINE.json): pins processed per second per coarsening level. One "step" is
+one pass of the whole hot path over one synthetic input:
+    a1 hgp_build_csr -> a2 hgp_unique_neighbors -> hgp_coarsen_level (a3 score, a4 match, a5 contract)
+on the level-0 hypergraph of the configured workload (default C2: SNN-mapping, 1M neurons,
+1e8 pins, Omega=256, Delta=4096, Pi=4, noise on).
+
+  value : P / device time of the step (inputs resident in HBM; CUDA events, max over ranks)
+  e2e   : the same through the C-ABI with HOST inputs: per step the pinned-host -> device copy
+          of the input arrays and the device -> host read of gamma are inside the timed region
+  roofline: the dominant kernel's algorithmic bytes / its live CUDA-event
+          time over the timed region, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline: the CPU oracle (oracle/, single thread) on a bounded sample of the same recipe
+
+`--impl reference` times the oracle alone (the tier's reference arm) on a bounded sample.
+Multi-GPU (torchrun, N>1): every rank runs its own replica of the workload (weak scaling,
+no data-path collective yet).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import hgpgen  # noqa: E402
+
+METRIC = "pins/sec per coarsening level (a1..a5 on level 0)"
+UNIT = "pins/s"
+
+
+def _workload(name: str, seed: int):
+    w = hgpgen.WORKLOADS[name]
+    hg = w.make(seed)
+    omega = w.omega if w.omega > 0 else hgpgen.kway_omega(hg, w.extra.get("kway", 2))
+    cap = hgpgen.default_noise_cap(hg) if w.noise else 0
+    return w, hg, omega, w.delta, w.pi, cap
+
+
+def algorithmic_bytes(step: str, N, E, P, V, pi, Nc=0, Ec=0, Pc=0, Vc=0) -> int:
+    """Minimum bytes each step must move (every array element read once, every output written
+    once; gathers counted once per element) — SURVEY §8(d), restated in DESIGN.md §Roofline."""
+    if step == "a1":
+        return 12 * P + 36 * E + 24 * N
+    if step == "a2":
+        return 8 * P + 8 * E + 16 * N + 4 * V
+    if step == "a3":
+        return 4 * V + 8 * P + 20 * E + 28 * N + 16 * pi * N
+    if step == "a4":
+        return 16 * pi * N + 4 * N
+    if step == "a5":
+        return 16 * N + 4 * P + 20 * E + 8 * Pc + 20 * Ec + 4 * V + 4 * Vc + 28 * Nc
+    raise KeyError(step)
+
+
+KERNEL_STEP = {"validate": "a1", "check": "a1", "segsort": "a1", "inc_": "a1", "fill_mu": "a1", "max_deg": "a1",
+               "edge_pairs": "a2", "nbrs_": "a2", "nbr_": "a2", "score_": "a3", "round_": "a4", "jump_": "a4",
+               "fill_none": "a4"}
+
+
+def step_of(kernel: str) -> str:
+    for k, v in KERNEL_STEP.items():
+        if kernel.startswith(k):
+            return v
+    return "a5"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], None, set()
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.path)
+        loaded = [x for x in sm if mx and x > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks() -> tuple[float, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel: str, workload: str):
+    """dram read+write bytes per launch of `kernel` from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    rec = d.get(workload, {}).get(kernel)
+    return rec.get("dram_bytes_per_launch") if rec else None
+
+
+# ------------------------------------------------------------------------------------------ oracle legs
+def oracle_level_seconds(hg, omega, delta, pi, cap, seed) -> float:
+    from oracle import ref
+    t0 = time.perf_counter()
+    g = ref.build_csr_hg(hg)
+    nb = ref.unique_neighbors(g)
+    ref.coarsen_level(g, nb, ref.params(omega, delta, pi, noise_seed=seed, noise_cap=cap))
+    return time.perf_counter() - t0
+
+
+def oracle_sample(workload: str, seed: int, scale: str):
+    """A bounded sample of the workload's recipe for the single-threaded oracle."""
+    if workload.startswith("C2") or workload == "C5":
+        rows, cols = (50, 80) if scale == "baseline" else (25, 40)
+        rew = 0.1 if workload == "C2r" else 0.0
+        hg = hgpgen.snn(seed, rows=rows, cols=cols, rewire=rew)
+        desc = f"SNN recipe (C2 generator) at 10 layers x {rows}x{cols} = {10 * rows * cols} neurons, " \
+               f"{hg.num_pins} pins; full level a1..a5"
+        return hg, 256, 4096, desc
+    n = 400_000 if scale == "baseline" else 100_000
+    hg = hgpgen.vlsi(seed, n, n)
+    om = 256 if workload == "C3" else hgpgen.kway_omega(hg)
+    de = 4096 if workload == "C3" else hgpgen.UNBOUNDED
+    return hg, om, de, f"VLSI recipe at {n} nodes/edges, {hg.num_pins} pins; full level a1..a5"
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    hg, om, de, desc = oracle_sample(args.workload, args.seed, "reference")
+    cap = hgpgen.default_noise_cap(hg)
+    for _ in range(args.warmup):
+        oracle_level_seconds(hg, om, de, 4, cap, args.seed)
+    ts = [oracle_level_seconds(hg, om, de, 4, cap, args.seed) for _ in range(args.steps)]
+    t = sum(ts) / len(ts)
+    value = hg.num_pins / t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64", "data": "synthetic",
+            "config": {"workload": hgpgen.WORKLOADS[args.workload].name, "sample": desc},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="hgp", choices=["hgp", "reference"])
+    ap.add_argument("--workload", default="C2", choices=sorted(hgpgen.WORKLOADS))
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dominant", default=None, help="kernel name for the roofline (default: measured top kernel)")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2605_20497_b200 import hgp
+
+    assert args.warmup >= 3 or os.environ.get("HGP_BENCH_ALLOW_SHORT"), "timing rules need >= 3 warm-up steps"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w, hg, omega, delta, pi, cap = _workload(args.workload, args.seed)
+    N, E, P = hg.num_nodes, hg.num_edges, hg.num_pins
+    stream = torch.cuda.current_stream()
+    ctx = hgp.Ctx(local, stream=stream)
+    host = {k: torch.from_numpy(np.ascontiguousarray(getattr(hg, k))).pin_memory()
+            for k in ("edge_off", "edge_nsrc", "pins", "edge_w", "node_w")}
+    dev = {k: v.cuda() for k, v in host.items()}
+    h2d_bytes = sum(v.numel() * v.element_size() for v in host.values())
+    params = hgp.params(omega, delta, pi, noise_seed=args.seed, noise_cap=cap)
+    cand = hgp.empty_cand(N, pi)
+    match = torch.empty(N, dtype=torch.uint32, device="cuda")
+    gamma = torch.empty(N, dtype=torch.uint32, device="cuda")
+    gamma_host = torch.empty(N, dtype=torch.uint32).pin_memory()
+
+    last = {}
+
+    def step(inp):
+        g = hgp.build_csr(ctx, N, inp["edge_off"], inp["edge_nsrc"], inp["pins"], inp["edge_w"], inp["node_w"])
+        nb = hgp.unique_neighbors(ctx, g)
+        cg, cnb, st = hgp.coarsen_level(ctx, g, nb, params, cand, match, gamma)
+        last.update(st=st, V=nb.V, max_deg=nb.c.max_deg)
+        for x in (g, nb, cg, cnb):
+            x.free()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step(dev)
+    torch.cuda.synchronize()
+
+    # ---- per-kernel breakdown (one untimed, profiled step) -> dominant kernel
+    ctx.profile_begin("")
+    step(dev)
+    ctx.profile_end()
+    breakdown = ctx.profile_report()
+    dominant = args.dominant or max(breakdown, key=lambda k: breakdown[k][0])
+
+    # ---- timed region: K steps, inputs resident in HBM (420 MB > 126 MB L2)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    l0 = ctx.launches
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.profile_begin(dominant)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(dev)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dom_ms, dom_launches = ctx.profile_end()
+    barrier()
+    launches = ctx.launches - l0
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    clk = clocks.stop()
+
+    # ---- end-to-end through the C-ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        bufs = {k: torch.empty_like(v) for k, v in dev.items()}
+
+        def step_e2e():
+            for k in bufs:
+                ctx.copy(bufs[k].data_ptr(), host[k].data_ptr(), host[k].numel() * host[k].element_size())
+            step(bufs)
+            ctx.copy(gamma_host.data_ptr(), gamma.data_ptr(), 4 * N)
+
+        step_e2e()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_e2e()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        e2e = {"value": world * P / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": 4 * N}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    st = last["st"]
+    V = last["V"]
+    dstep = step_of(dominant)
+    alg = algorithmic_bytes(dstep, N, E, P, V, pi, st["Nc"], st["Ec"], st["Pc"], st["Vc"])
+    per_launch_ms = dom_ms / max(dom_launches, 1)
+    # bytes per launch: the step's bytes split over that step's launches of this kernel per step
+    launches_per_step = max(dom_launches / args.steps, 1)
+    achieved = (alg / launches_per_step) / (per_launch_ms * 1e-3) / 1e9
+    peak, peak_kind = measured_peaks()
+    step_ms = {}
+    for k, (kms, _) in breakdown.items():
+        step_ms[step_of(k)] = step_ms.get(step_of(k), 0.0) + kms
+    line = {
+        "metric": METRIC, "value": world * P / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32/u64 (integer fixed point)", "data": "synthetic",
+        "config": {"workload": w.name, "N": N, "E": E, "P": P, "V": V, "omega": omega,
+                   "delta": "inf" if delta == hgpgen.UNBOUNDED else delta, "pi": pi, "noise_cap": cap,
+                   "seed": args.seed, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "inputs (%.0f MB) larger than L2" % (h2d_bytes / 1e6)},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "roofline": {"bound": "hbm", "kernel": dominant, "step": dstep, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "alg_bytes_per_launch": alg / launches_per_step, "ms_per_launch": per_launch_ms,
+                     "traffic": ncu_traffic(dominant, args.workload)},
+        "level": {"Nc": st["Nc"], "Ec": st["Ec"], "Pc": st["Pc"], "Vc": st["Vc"],
+                  "matched_fraction": 2 * sum(st["matched_per_round"]) / N,
+                  "matched_per_round": st["matched_per_round"], "purged": st["purged"],
+                  "merged_edges": st["merged_edges"], "dropped_edges": st["dropped_edges"]},
+        "step_ms": {k: round(v, 4) for k, v in sorted(step_ms.items())},
+        "kernels_ms": {k: round(v[0], 4) for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])[:12]},
+        "level_hbm_frac": sum(algorithmic_bytes(s, N, E, P, V, pi, st["Nc"], st["Ec"], st["Pc"], st["Vc"])
+                              for s in ("a1", "a2", "a3", "a4", "a5")) / (ms * 1e-3) / 1e9 / peak,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        hs, om, de, desc = oracle_sample(args.workload, args.seed, "baseline")
+        t = oracle_level_seconds(hs, om, de, pi, hgpgen.default_noise_cap(hs), args.seed)
+        line["cpu_baseline"] = {"value": hs.num_pins / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": desc, "seconds": t, "host_cores": os.cpu_count()}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

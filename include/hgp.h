@@ -1,0 +1,200 @@
+/* hgp.h — C-ABI of the B200-native coarsening level (arXiv 2605.20497, §5).
+ *
+ * One coarsening level of a weighted directed hypergraph under a size limit Omega
+ * and a distinct-inbound-hyperedge limit Delta, as five steps:
+ *   a1 hgp_build_csr        compressed sparse layout, src-first / in-first
+ *   a2 hgp_unique_neighbors materialised unique neighbourhoods N(n)
+ *   a3 hgp_score_pairs      histogram eta + inline intersection + validity + noise
+ *                           + purge flags + top-Pi candidates (Eqs.5-6)
+ *   a4 hgp_match            exact DP matching on Pi two-cycle pseudo-forests (Eqs.7-12)
+ *   a5 hgp_contract         gamma + coarse hyperedges/incidence/neighbours
+ * and hgp_coarsen_level = a3 -> a4 -> a5 on one level.
+ *
+ * Conventions
+ *  - Every pointer inside hgp_input / hgp_csr / hgp_nbrs / hgp_cand / match / gamma is a
+ *    DEVICE pointer on the ctx's device. Host pointers appear only where stated.
+ *  - Ids are uint32; HGP_NONE marks "undefined". Node count N < 2^31 (bit 31 of a
+ *    neighbour entry is the purge flag).
+ *  - Scores are unsigned fixed point with HGP_FP_SHIFT fraction bits: the Eq.5 term of
+ *    an edge is c(e) = floor(omega(e) * 2^24 / |e|) (norm = 0) or omega(e) * 2^24 (norm = 1).
+ *    All sums are exact integers, so results do not depend on the parallel schedule.
+ *  - Ownership: inputs are borrowed (they must stay alive until the stream passes the
+ *    call); fixed-size outputs (cand, match, gamma) are caller-allocated; data-dependent
+ *    outputs (hgp_csr, hgp_nbrs arrays) are allocated by the library through the ctx's
+ *    allocator and released with hgp_csr_free / hgp_nbrs_free.
+ *  - Order inside a segment: hyperedge src/dst blocks and incidence in/out lists are
+ *    ascending (canonical). Neighbour segments are SETS (ascending order is not
+ *    guaranteed; the paper builds them with hash sets); compare them as sets.
+ *  - Errors: every call returns an hgp_status; the first error wins and
+ *    hgp_last_error() (thread-local) names the lowest offending edge/node index.
+ *    No exceptions and no host fallback: without a CUDA device every call fails.
+ *  - Synchronisation: hgp_build_csr, hgp_unique_neighbors, hgp_contract and
+ *    hgp_coarsen_level synchronise the ctx stream (scan totals size their outputs);
+ *    hgp_score_pairs and hgp_match only enqueue work (device-side errors of a4 are
+ *    reported by the next synchronising call on the same ctx).
+ */
+#ifndef HGP_H
+#define HGP_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(_WIN32)
+#define HGP_API
+#else
+#define HGP_API __attribute__((visibility("default")))
+#endif
+
+#define HGP_NONE 0xFFFFFFFFu
+#define HGP_UNBOUNDED UINT64_MAX          /* Omega or Delta = +inf (k-way: Delta) */
+#define HGP_FP_SHIFT 24
+#define HGP_PURGE 0x80000000u             /* neighbour entry flag: permanently invalid */
+#define HGP_MAX_PI 16
+
+typedef enum {
+  HGP_OK = 0,
+  HGP_E_ARG = -1,         /* bad argument (null pointer, range, parameter out of domain) */
+  HGP_E_MALFORMED = -2,   /* input violates P:290-297: pin >= N, duplicate pin, src∩dst != ∅,
+                             empty edge, omega = 0, size = 0, non-monotone offsets, nsrc > |e| */
+  HGP_E_INFEASIBLE = -3,  /* a node alone exceeds Omega or Delta: no valid solution */
+  HGP_E_OVERFLOW = -4,    /* N >= 2^31, |e| > 2^24, sum omega >= 2^32, sum size >= 2^32,
+                             or score totals that could reach 2^62 */
+  HGP_E_OOM = -5,         /* the allocator returned NULL */
+  HGP_E_CUDA = -6,        /* CUDA runtime error (message carries cudaGetErrorString) */
+  HGP_E_NCCL = -7,        /* reserved for the library-internal NCCL path */
+  HGP_E_INTERNAL = -8     /* broken invariant, e.g. a proposal cycle longer than 2 */
+} hgp_status;
+
+typedef struct CUstream_st *hgp_stream_t;   /* == cudaStream_t */
+
+/* Device allocator. alloc returns a device pointer (NULL on failure); free releases it.
+ * Both are called on the host thread that issued the hgp_* call, with the ctx stream.
+ * Passing NULL to hgp_ctx_create selects the built-in stream-ordered pool (cudaMallocAsync). */
+typedef struct {
+  void *(*alloc)(void *user, size_t bytes, hgp_stream_t stream);
+  void (*free)(void *user, void *ptr, size_t bytes, hgp_stream_t stream);
+  void *user;
+} hgp_allocator;
+
+typedef struct hgp_ctx hgp_ctx;             /* opaque: device, stream, allocator, scratch arena */
+
+/* Problem statement. DEVICE pointers, borrowed. */
+typedef struct {
+  uint32_t num_nodes, num_edges;
+  const uint64_t *edge_off;   /* [E+1] edge_off[0] = 0, nondecreasing; |e| = off[e+1]-off[e] >= 1 */
+  const uint32_t *edge_nsrc;  /* [E]   the first nsrc pins of edge e are src(e), the rest dst(e) */
+  const uint32_t *pins;       /* [P]   node ids < N, any order inside the src / dst blocks */
+  const uint32_t *edge_w;     /* [E]   omega(e) >= 1, sum < 2^32 */
+  const uint32_t *node_w;     /* [N]   size(n) >= 1, sum < 2^32 */
+} hgp_input;
+
+/* One level. Library-owned DEVICE arrays; scalar fields are host values. */
+typedef struct {
+  uint32_t N, E;
+  uint64_t P;                 /* number of pins = sum |e| = sum |I(n)| */
+  uint32_t max_edge;          /* max |e| (host-known, selects kernel tiers) */
+  uint32_t max_inc;           /* max |I(n)| */
+  uint64_t *edge_off;         /* [E+1] */
+  uint32_t *edge_nsrc;        /* [E]   |src(e)| */
+  uint32_t *pins;             /* [P]   src(e) ascending ‖ dst(e) ascending */
+  uint32_t *edge_w;           /* [E]   omega(e) (coarse: sum over merged edges) */
+  uint32_t *edge_mu;          /* [E]   inbound multiplicity: original edges merged into e */
+  uint32_t *node_w;           /* [N]   size(n) */
+  uint64_t *inc_off;          /* [N+1] */
+  uint32_t *inc_nin;          /* [N]   |in(n)| */
+  uint32_t *inc;              /* [P]   in(n) ascending ‖ out(n) ascending (edge ids) */
+  uint32_t *in_mu;            /* [N]   sum of mu(e) over in(n) = distinct original inbound edges */
+} hgp_csr;
+
+/* Materialised neighbours of nodes lo..hi-1. Library-owned DEVICE arrays. */
+typedef struct {
+  uint32_t lo, hi;
+  uint64_t V;                 /* entries */
+  uint32_t max_deg;           /* max |N(n)| over the range (host-known) */
+  uint32_t pad_;
+  uint64_t *off;              /* [hi-lo+1], off[0] = 0 */
+  uint32_t *nbr;              /* [V]   node id | HGP_PURGE flag; each segment is a set */
+} hgp_nbrs;
+
+/* Candidate: node-major [N][pi]; unused slots id = HGP_NONE, score = 0. */
+typedef struct { uint32_t id, pad; uint64_t score; } hgp_cand;
+
+typedef struct {
+  uint64_t omega, delta;      /* Omega, Delta (HGP_UNBOUNDED allowed); validity uses <= */
+  uint32_t pi;                /* Pi in [1, 16]; the paper's default is 4 */
+  uint32_t norm;              /* 0: Eq.5 omega/|e| (default); 1: raw omega */
+  uint64_t noise_seed;        /* deterministic symmetric noise */
+  uint64_t noise_cap;         /* noise in [0, cap], 2^-24 units; 0 disables; cap < 2^56 */
+  uint32_t batch;             /* tuning only; results never depend on it */
+  uint32_t flags;             /* reserved, 0 */
+} hgp_params;
+
+typedef struct {
+  uint32_t N, E, Nc, Ec;
+  uint64_t P, V, Pc, Vc;
+  uint32_t matched_per_round[HGP_MAX_PI];
+  uint32_t dropped_edges, merged_edges;
+  uint64_t purged;            /* entries flagged by a3 in this level */
+  float ms[4];                /* device time: score, match, contract, total (CUDA events) */
+} hgp_level_stats;
+
+/* ---- context ---------------------------------------------------------------------------- */
+/* device: CUDA ordinal; stream: NULL = the legacy default stream; alloc: NULL = built-in pool. */
+HGP_API hgp_status hgp_ctx_create(int device, hgp_stream_t stream, const hgp_allocator *alloc, hgp_ctx **out);
+HGP_API void hgp_ctx_destroy(hgp_ctx *ctx);
+HGP_API const char *hgp_last_error(void);
+/* number of kernels this ctx has launched so far (for the bench's gpu_launches claim) */
+HGP_API uint64_t hgp_launch_count(const hgp_ctx *ctx);
+/* stream-ordered copy on the ctx stream, cudaMemcpyDefault semantics (host or device pointers);
+ * synchronises the stream when either side is pageable host memory. */
+HGP_API hgp_status hgp_copy(hgp_ctx *ctx, void *dst, const void *src, size_t bytes);
+HGP_API hgp_status hgp_sync(hgp_ctx *ctx);
+/* Instrumentation: from hgp_profile_begin on, every kernel launch whose internal name contains
+ * name_filter (e.g. "score_A") is bracketed by CUDA events on the ctx stream; hgp_profile_end
+ * synchronises and returns the summed device time (ms) and the number of such launches. */
+HGP_API hgp_status hgp_profile_begin(hgp_ctx *ctx, const char *name_filter);
+HGP_API hgp_status hgp_profile_end(hgp_ctx *ctx, double *total_ms, uint64_t *launches);
+/* After hgp_profile_end: per kernel name "name:ms:launches;" into the HOST buffer buf. */
+HGP_API hgp_status hgp_profile_report(hgp_ctx *ctx, char *buf, size_t len);
+
+/* ---- the level's steps ------------------------------------------------------------------ */
+/* a1: validate the input and build the canonical level-0 CSR (mu = 1). Synchronises. */
+HGP_API hgp_status hgp_build_csr(hgp_ctx *ctx, const hgp_input *in, hgp_csr *out);
+
+/* a2: N(n) = (U_{e in I(n)} e) \ {n} for n in [lo, hi), purge bits clear. Synchronises. */
+HGP_API hgp_status hgp_unique_neighbors(hgp_ctx *ctx, const hgp_csr *g, uint32_t lo, uint32_t hi,
+                                        hgp_nbrs *out);
+
+/* a3: for n in [nb->lo, nb->hi): eta/inter histogram over unflagged N(n), validity, noise,
+ * purge flags set IN PLACE on nb (idempotent), top-pi valid neighbours by (score desc, id desc)
+ * into cand rows lo..hi-1 of a caller [N][pi] array. Asynchronous. */
+HGP_API hgp_status hgp_score_pairs(hgp_ctx *ctx, const hgp_csr *g, hgp_nbrs *nb, const hgp_params *p,
+                                   hgp_cand *cand);
+
+/* a4: pi rounds of exact matching; match[N] symmetric partner or HGP_NONE;
+ * matched_per_round: DEVICE [pi] pairs matched per round, or NULL. Asynchronous. */
+HGP_API hgp_status hgp_match(hgp_ctx *ctx, const hgp_cand *cand, uint32_t N, uint32_t pi,
+                             uint32_t *match, uint32_t *matched_per_round);
+
+/* a5: gamma[N] (coarse ids by ascending min member) and the coarse level: merged parallel
+ * edges (omega' = sum omega, mu' = sum mu, ordered by min fine edge id), canonical incidence,
+ * coarse neighbours = gamma(N(a) ∪ N(b)) minus OR-propagated purged entries minus self.
+ * nb must cover every node. Synchronises. */
+HGP_API hgp_status hgp_contract(hgp_ctx *ctx, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match,
+                                uint32_t *gamma, hgp_csr *coarse, hgp_nbrs *coarse_nb);
+
+/* a3 -> a4 -> a5 on one level. cand may be NULL (scratch). stats (HOST pointer) may be NULL. */
+HGP_API hgp_status hgp_coarsen_level(hgp_ctx *ctx, const hgp_csr *g, hgp_nbrs *nb, const hgp_params *p,
+                                     hgp_cand *cand, uint32_t *match, uint32_t *gamma, hgp_csr *coarse,
+                                     hgp_nbrs *coarse_nb, hgp_level_stats *stats);
+
+HGP_API void hgp_csr_free(hgp_ctx *ctx, hgp_csr *g);
+HGP_API void hgp_nbrs_free(hgp_ctx *ctx, hgp_nbrs *nb);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HGP_H */

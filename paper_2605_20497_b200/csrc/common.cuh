@@ -1,0 +1,197 @@
+// common.cuh — context, errors, launches, scratch arena and small device helpers.
+// Part of the product path (libhgp.so); shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "hgp.h"
+
+namespace hgp {
+
+constexpr uint32_t kNone = HGP_NONE;
+constexpr uint32_t kPurge = HGP_PURGE;
+constexpr uint32_t kIdMask = 0x7FFFFFFFu;
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;   // empty hash slot
+constexpr int kWarp = 32;
+
+hgp_status set_error(hgp_status code, const char *fmt, ...);
+
+// Device-side error slots: the lowest offending index per category (atomicMin).
+enum ErrSlot : int {
+  kErrStruct = 0,     // offsets / empty edge / nsrc > |e|
+  kErrEdgeBig = 1,    // |e| > 2^24 (overflow)
+  kErrPinRange = 2,
+  kErrDup = 3,
+  kErrEdgeW = 4,
+  kErrNodeW = 5,
+  kErrInfeasW = 6,    // node size > Omega
+  kErrInfeasD = 7,    // node in_mu > Delta
+  kErrCycle = 8,      // proposal cycle longer than 2 (a4)
+  kErrInternal = 9,
+  kErrSlots = 16
+};
+
+}  // namespace hgp
+
+struct hgp_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  hgp_allocator alloc{};
+  bool builtin_pool = false;
+  // scratch arena (reset at every top-level API call)
+  struct Chunk { void *p; size_t bytes; };
+  std::vector<Chunk> chunks;
+  size_t used = 0;       // bytes used in chunks.back()
+  int depth = 0;
+  uint64_t launches = 0;
+  uint64_t *d_err = nullptr;       // [kErrSlots] device
+  uint64_t *h_pin = nullptr;       // [64] pinned host staging
+  cudaEvent_t ev[8] = {};
+  // profiling: CUDA events around every launch whose name contains prof_filter
+  std::string prof_filter;
+  bool prof_on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+  std::vector<const char *> prof_names;
+  std::vector<cudaEvent_t> prof_pool;
+  cudaEvent_t prof_event();
+
+  void *dalloc(size_t bytes);
+  void dfree(void *p, size_t bytes);
+  void *scratch(size_t bytes);     // 256-byte aligned, valid until the next top-level call
+  void reset_scratch();
+};
+
+namespace hgp {
+
+// RAII guard for top-level API entry points: resets scratch at depth 0.
+struct ApiScope {
+  hgp_ctx *c;
+  explicit ApiScope(hgp_ctx *c_) : c(c_) {
+    if (c->depth++ == 0) c->reset_scratch();
+  }
+  ~ApiScope() { --c->depth; }
+};
+
+#define HGP_CUDA(x)                                                                              \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess)                                                                       \
+      return ::hgp::set_error(HGP_E_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, \
+                              __LINE__);                                                         \
+  } while (0)
+
+#define HGP_TRY(x)                     \
+  do {                                 \
+    hgp_status s_ = (x);               \
+    if (s_ != HGP_OK) return s_;       \
+  } while (0)
+
+template <class K, class... Args>
+inline hgp_status launch(hgp_ctx *c, const char *name, K kernel, dim3 grid, dim3 block, size_t smem,
+                         Args... args) {
+  if (grid.x == 0 || grid.y == 0 || grid.z == 0) return HGP_OK;
+  const bool prof = c->prof_on && strstr(name, c->prof_filter.c_str()) != nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof) { e0 = c->prof_event(); e1 = c->prof_event(); cudaEventRecord(e0, c->stream); }
+  kernel<<<grid, block, smem, c->stream>>>(args...);
+  if (prof) { cudaEventRecord(e1, c->stream); c->prof_events.push_back({e0, e1}); c->prof_names.push_back(name); }
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(HGP_E_CUDA, "launch %s: %s", name, cudaGetErrorString(e));
+  return HGP_OK;
+}
+
+// Allocate zero-initialised scratch.
+template <class T>
+inline T *scratch_zero(hgp_ctx *c, size_t n, hgp_status *st) {
+  T *p = static_cast<T *>(c->scratch(sizeof(T) * (n ? n : 1)));
+  if (!p) { *st = set_error(HGP_E_OOM, "scratch allocation of %zu bytes failed", sizeof(T) * n); return nullptr; }
+  cudaError_t e = cudaMemsetAsync(p, 0, sizeof(T) * (n ? n : 1), c->stream);
+  if (e != cudaSuccess) { *st = set_error(HGP_E_CUDA, "memset: %s", cudaGetErrorString(e)); return nullptr; }
+  return p;
+}
+template <class T>
+inline T *scratch_raw(hgp_ctx *c, size_t n, hgp_status *st) {
+  T *p = static_cast<T *>(c->scratch(sizeof(T) * (n ? n : 1)));
+  if (!p) *st = set_error(HGP_E_OOM, "scratch allocation of %zu bytes failed", sizeof(T) * n);
+  return p;
+}
+template <class T>
+inline T *dalloc_n(hgp_ctx *c, size_t n, hgp_status *st) {
+  T *p = static_cast<T *>(c->dalloc(sizeof(T) * (n ? n : 1)));
+  if (!p) *st = set_error(HGP_E_OOM, "device allocation of %zu bytes failed", sizeof(T) * n);
+  return p;
+}
+
+// Read device scalars into host (synchronises the ctx stream).
+hgp_status read_back(hgp_ctx *c, const void *dptr, size_t bytes, void *host);
+inline hgp_status read_u64(hgp_ctx *c, const uint64_t *d, uint64_t *h) { return read_back(c, d, 8, h); }
+
+// Reset / read the device error slots.
+hgp_status clear_errors(hgp_ctx *c);
+hgp_status fetch_errors(hgp_ctx *c, uint64_t out[kErrSlots]);
+
+inline uint32_t div_up(uint64_t a, uint64_t b) { return static_cast<uint32_t>((a + b - 1) / b); }
+
+// ---------------------------------------------------------------------------- device helpers
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+inline uint64_t splitmix64_host(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Multiplicative (Fibonacci) hash of a node id into a power-of-two table.
+__device__ __forceinline__ uint32_t hash_slot(uint32_t key, uint32_t log2size) {
+  return (key * 0x9E3779B1u) >> (32u - log2size);
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+// inclusive warp prefix sum
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T w = __shfl_up_sync(0xFFFFFFFFu, v, o);
+    if (lane >= (uint32_t)o) v += w;
+  }
+  return v;
+}
+
+__device__ __forceinline__ void report_min(uint64_t *err, int slot, uint64_t idx) {
+  atomicMin(reinterpret_cast<unsigned long long *>(err + slot), static_cast<unsigned long long>(idx));
+}
+
+}  // namespace hgp

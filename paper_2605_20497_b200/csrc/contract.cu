@@ -1,0 +1,498 @@
+// contract.cu — a5: coarse hypergraph construction (§5.5; §3).
+//
+//  gamma   rep(n) <=> match(n) = NONE or n < match(n); coarse id = exclusive scan of rep
+//          (ascending min member); gamma(n) = cid(min(n, match(n))); size' = sum of sizes.
+//  edges   per fine edge (in its own oversized slot): map pins by gamma, sort the
+//          src and dst blocks, D' = unique dst, S' = unique src \ D' (duplicates kept in dst,
+//          P:831); dropped iff D' empty and |S'| <= 1 (reading #14).
+//  merge   parallel edges (identical (S',D')) are found through a global hash table keyed by a
+//          64-bit fingerprint and verified element by element; the class representative is the
+//          minimum fine edge id (atomicMin), omega' = sum omega, mu' = sum mu (reading #12);
+//          coarse edges are ordered by representative.
+//  incid.  rebuilt by the a1 transpose (canonical in-first lists, in_mu' = sum mu').
+//  N'      per coarse node: gamma(N(a) ∪ N(b)) in a hash set with an OR-ed purge flag per key;
+//          flagged keys and the node itself are dropped (reading #7).
+#include "csr_impl.cuh"
+#include "hashset.cuh"
+#include "lbs.cuh"
+#include "scan.cuh"
+#include "sort.cuh"
+
+namespace hgp {
+
+constexpr int kErrMatch = 10;
+
+__global__ void k_rep(const uint32_t *match, uint32_t N, uint32_t *rep, uint64_t *err) {
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    const uint32_t m = match[n];
+    if (m != kNone && (m >= N || m == n || match[m] != n)) report_min(err, kErrMatch, n);
+    rep[n] = (m == kNone || n < m) ? 1u : 0u;
+  }
+}
+
+__global__ void k_gamma(const uint32_t *match, const uint64_t *cid, const uint32_t *node_w, uint32_t N,
+                        uint32_t *gamma, uint32_t *cw, uint32_t *mem0, uint32_t *mem1) {
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    const uint32_t m = match[n];
+    const uint32_t lo = (m == kNone || n < m) ? n : m;
+    const uint32_t c = (uint32_t)cid[lo];
+    gamma[n] = c;
+    atomicAdd(&cw[c], node_w[n]);
+    if (lo == n) { mem0[c] = n; mem1[c] = m; }
+  }
+}
+
+__global__ void __launch_bounds__(kLbsThreads) k_map_pins(const uint32_t *pins, const uint32_t *gamma, uint64_t P,
+                                                          uint32_t *out) {
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (uint64_t)gridDim.x * blockDim.x)
+    out[p] = gamma[pins[p]];
+}
+
+struct EdgeSeg2 {   // segment 2e = src(e), 2e+1 = dst(e) of the fine layout
+  const uint64_t *off;
+  const uint32_t *nsrc;
+  __device__ void operator()(uint64_t i, uint64_t &beg, uint32_t &len) const {
+    const uint64_t e = i >> 1;
+    const uint64_t lo = off[e], hi = off[e + 1], s = lo + nsrc[e];
+    if (i & 1) { beg = s; len = (uint32_t)(hi - s); }
+    else { beg = lo; len = (uint32_t)(s - lo); }
+  }
+};
+
+__device__ __forceinline__ uint64_t fp_mix(uint64_t h, uint32_t x, uint32_t i) {
+  return h + splitmix64(((uint64_t)x << 32) ^ (uint64_t)i * 0xD6E8FEB86659FD93ull);
+}
+
+// Unique + src\dst filtering in place; layout [S'][D'] from off[e]; warp per edge.
+__global__ void k_edge_unique(const uint64_t *off, const uint32_t *nsrc, uint32_t E, uint32_t *x, uint32_t *cnsrc,
+                              uint32_t *csize, uint8_t *keep, uint64_t *fp) {
+  const uint32_t lane = lane_id();
+  const uint32_t lt = (1u << lane) - 1;
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t e = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < E; e += nw) {
+    const uint64_t lo = off[e], hi = off[e + 1], s = lo + nsrc[e];
+    // S' = unique src not present in the (sorted) dst block
+    uint32_t ns = 0;
+    uint32_t prev = kNone;   // last element of the previous chunk
+    for (uint64_t base = lo; base < s; base += 32) {
+      const uint64_t j = base + lane;
+      uint32_t v = j < s ? x[j] : kNone;
+      const uint32_t before = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+      const uint32_t left = lane == 0 ? prev : before;
+      bool k = j < s && v != left;
+      if (k) {
+        uint64_t a = s, b = hi;
+        while (a < b) {
+          const uint64_t m = (a + b) >> 1;
+          if (x[m] < v) a = m + 1; else b = m;
+        }
+        if (a < hi && x[a] == v) k = false;
+      }
+      prev = __shfl_sync(0xFFFFFFFFu, v, 31);
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, k);
+      __syncwarp();
+      if (k) x[lo + ns + __popc(bal & lt)] = v;
+      ns += __popc(bal);
+      __syncwarp();
+    }
+    // D' = unique dst, moved to lo + ns (never overtakes the read position: ns <= s - lo)
+    uint32_t nd = 0;
+    prev = kNone;
+    for (uint64_t base = s; base < hi; base += 32) {
+      const uint64_t j = base + lane;
+      const uint32_t v = j < hi ? x[j] : kNone;
+      const uint32_t before = __shfl_up_sync(0xFFFFFFFFu, v, 1);
+      const uint32_t left = lane == 0 ? prev : before;
+      const bool k = j < hi && v != left;
+      prev = __shfl_sync(0xFFFFFFFFu, v, 31);
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, k);
+      __syncwarp();
+      if (k) x[lo + ns + nd + __popc(bal & lt)] = v;
+      nd += __popc(bal);
+      __syncwarp();
+    }
+    const bool kp = !(nd == 0 && ns <= 1);
+    // fingerprint of (|S'|, S', D')
+    uint64_t h = 0;
+    if (kp)
+      for (uint32_t i = lane; i < ns + nd; i += 32) h = fp_mix(h, x[lo + i], i);
+    h = warp_sum(h);
+    if (lane == 0) {
+      cnsrc[e] = ns;
+      csize[e] = ns + nd;
+      keep[e] = kp;
+      fp[e] = splitmix64(h ^ ((uint64_t)ns << 40) ^ (uint64_t)(ns + nd));
+    }
+  }
+}
+
+struct MergeJob {
+  const uint64_t *off;
+  const uint32_t *x, *cnsrc, *csize;
+  const uint8_t *keep;
+  const uint64_t *fp;
+  uint32_t E;
+  uint32_t *owner;     // table slots: edge id of the first inserter (kEmpty = free)
+  uint32_t *minrep;    // per slot: min edge id of the class
+  uint32_t *slot_of;   // per edge
+  uint32_t log2t;
+};
+
+__device__ __forceinline__ bool same_edge(const MergeJob &M, uint32_t a, uint32_t b) {
+  if (M.fp[a] != M.fp[b] || M.cnsrc[a] != M.cnsrc[b] || M.csize[a] != M.csize[b]) return false;
+  const uint32_t *pa = M.x + M.off[a], *pb = M.x + M.off[b];
+  for (uint32_t i = 0; i < M.csize[a]; ++i)
+    if (pa[i] != pb[i]) return false;
+  return true;
+}
+
+__global__ void k_merge_insert(MergeJob M) {
+  const uint32_t mask = (1u << M.log2t) - 1;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < M.E; e += gridDim.x * blockDim.x) {
+    if (!M.keep[e]) continue;
+    uint32_t slot = (uint32_t)(M.fp[e] >> 7) & mask;
+    while (true) {
+      uint32_t o = *(volatile uint32_t *)&M.owner[slot];
+      if (o == kEmpty) {
+        o = atomicCAS(&M.owner[slot], kEmpty, e);
+        if (o == kEmpty) break;
+      }
+      if (same_edge(M, o, e)) break;
+      slot = (slot + 1) & mask;
+    }
+    M.slot_of[e] = slot;
+    atomicMin(&M.minrep[slot], e);
+  }
+}
+
+__global__ void k_merge_resolve(MergeJob M, uint32_t *rep, uint32_t *is_rep) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < M.E; e += gridDim.x * blockDim.x) {
+    const uint32_t r = M.keep[e] ? M.minrep[M.slot_of[e]] : kNone;
+    rep[e] = r;
+    is_rep[e] = r == e;
+  }
+}
+
+__global__ void k_coarse_edge_attrs(const uint32_t *rep, const uint64_t *ceid, const uint32_t *edge_w,
+                                    const uint32_t *edge_mu, const uint32_t *cnsrc, const uint32_t *csize, uint32_t E,
+                                    uint32_t *cw, uint32_t *cmu, uint32_t *c_nsrc, uint32_t *c_size) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const uint32_t r = rep[e];
+    if (r == kNone) continue;
+    const uint32_t ce = (uint32_t)ceid[r];
+    atomicAdd(&cw[ce], edge_w[e]);
+    atomicAdd(&cmu[ce], edge_mu[e]);
+    if (r == e) { c_nsrc[ce] = cnsrc[e]; c_size[ce] = csize[e]; }
+  }
+}
+
+__global__ void k_coarse_edge_pack(const uint32_t *rep, const uint64_t *ceid, const uint64_t *off, const uint32_t *x,
+                                   const uint32_t *csize, const uint64_t *coff, uint32_t E, uint32_t *cpins,
+                                   unsigned int *maxe) {
+  const uint32_t lane = lane_id();
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  uint32_t mx = 0;
+  for (uint64_t e = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < E; e += nw) {
+    if (rep[e] != e) continue;
+    const uint32_t n = csize[e];
+    const uint32_t *src = x + off[e];
+    uint32_t *dst = cpins + coff[ceid[e]];
+    for (uint32_t i = lane; i < n; i += 32) dst[i] = src[i];
+    mx = max(mx, n);
+  }
+  mx = warp_max(mx);
+  if (lane == 0) atomicMax(maxe, mx);
+}
+
+// ---------------------------------------------------------------- coarse neighbours
+struct CNbrJob {
+  const uint32_t *mem0, *mem1;
+  const uint64_t *nb_off;
+  const uint32_t *nbr;
+  const uint32_t *gamma;
+  const uint64_t *bound_off;   // exclusive scan of |N(a)|+|N(b)| (oversized slots)
+  uint32_t *pool;              // [V]
+  uint32_t *cnt;               // [Nc]
+  const uint32_t *list;        // coarse nodes for this tier (nullptr: all, filtered by cap)
+  const uint32_t *list_count;
+  uint32_t Nc;
+  uint32_t cap;                // tier capacity (entries)
+  uint32_t log2s;
+  uint32_t *gtab;              // global tables (keys | flags) when not in smem
+  unsigned long long *purged;
+};
+
+template <int THREADS, bool SMEM>
+__global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
+  extern __shared__ uint32_t dyn[];
+  __shared__ uint64_t wt[33];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t S = 1u << J.log2s;
+  uint32_t *keys = SMEM ? dyn : J.gtab + ((size_t)blockIdx.x << (J.log2s + 1));
+  uint32_t *flag = keys + S;
+  const uint32_t total = J.list_count ? *J.list_count : J.Nc;
+  uint64_t purged = 0;
+  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const uint32_t c = J.list ? J.list[t] : t;
+    const uint32_t a = J.mem0[c], b = J.mem1[c];
+    const uint64_t a0 = J.nb_off[a], a1 = J.nb_off[a + 1];
+    const uint64_t b0 = b == kNone ? 0 : J.nb_off[b], b1 = b == kNone ? 0 : J.nb_off[b + 1];
+    const uint64_t na = a1 - a0, nbn = b1 - b0;
+    if (!J.list && na + nbn > J.cap) continue;                      // larger tier (uniform)
+    for (uint32_t i = tid; i < S; i += THREADS) { keys[i] = kEmpty; flag[i] = 0; }
+    __syncthreads();
+    for (uint64_t k = tid; k < na + nbn; k += THREADS) {
+      const uint32_t v = k < na ? J.nbr[a0 + k] : J.nbr[b0 + (k - na)];
+      const uint32_t gm = J.gamma[v & kIdMask];
+      bool ins;
+      const uint32_t slot = hs_insert_slot(keys, J.log2s, gm, &ins);
+      if (v & kPurge) { flag[slot] = 1; ++purged; }
+    }
+    __syncthreads();
+    const uint32_t per = S / THREADS, base = tid * per;
+    uint64_t mine = 0;
+    for (uint32_t i = 0; i < per; ++i) {
+      const uint32_t k = keys[base + i];
+      mine += k != kEmpty && k != c && !flag[base + i];
+    }
+    uint64_t tot;
+    uint64_t pos = J.bound_off[c] + block_excl_scan<uint64_t>(mine, wt, &tot);
+    for (uint32_t i = 0; i < per; ++i) {
+      const uint32_t k = keys[base + i];
+      if (k != kEmpty && k != c && !flag[base + i]) J.pool[pos++] = k;
+    }
+    if (tid == 0) J.cnt[c] = (uint32_t)tot;
+    __syncthreads();
+  }
+  purged = warp_sum(purged);
+  if ((tid & 31) == 0 && purged) atomicAdd(J.purged, (unsigned long long)purged);
+}
+
+struct BoundIn {   // |N(a)| + |N(b)| per coarse node
+  const uint32_t *mem0, *mem1;
+  const uint64_t *nb_off;
+  __device__ uint64_t operator()(uint64_t c) const {
+    const uint32_t a = mem0[c], b = mem1[c];
+    return (nb_off[a + 1] - nb_off[a]) + (b == kNone ? 0 : nb_off[b + 1] - nb_off[b]);
+  }
+};
+
+__global__ void k_cnbr_classify(const uint64_t *bound_off, uint32_t Nc, uint32_t capA, uint32_t capB, uint32_t *listB,
+                                uint32_t *listC, uint32_t *counts, unsigned long long *maxb) {
+  uint64_t mx = 0;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < Nc; c += gridDim.x * blockDim.x) {
+    const uint64_t d = bound_off[c + 1] - bound_off[c];
+    if (d > capA) {
+      if (d <= capB) listB[atomicAdd(&counts[0], 1u)] = c;
+      else { listC[atomicAdd(&counts[1], 1u)] = c; mx = d > mx ? d : mx; }
+    }
+  }
+  mx = warp_max(mx);
+  if (lane_id() == 0 && mx) atomicMax(maxb, (unsigned long long)mx);
+}
+
+__global__ void k_cnbr_pack(const uint32_t *pool, const uint64_t *bound_off, const uint32_t *cnt, const uint64_t *off,
+                            uint32_t Nc, uint32_t *nbr, unsigned int *maxdeg) {
+  const uint32_t lane = lane_id();
+  uint32_t mx = 0;
+  for (uint32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < Nc; c += gridDim.x * (blockDim.x >> 5)) {
+    const uint32_t n = cnt[c];
+    const uint32_t *src = pool + bound_off[c];
+    uint32_t *dst = nbr + off[c];
+    for (uint32_t i = lane; i < n; i += 32) dst[i] = src[i];
+    mx = max(mx, n);
+  }
+  mx = warp_max(mx);
+  if (lane == 0) atomicMax(maxdeg, mx);
+}
+
+__global__ void k_count_kept(const uint32_t *rep, uint32_t E, uint32_t *out) {
+  uint32_t s = 0;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) s += rep[e] != kNone;
+  s = warp_sum(s);
+  if (lane_id() == 0 && s) atomicAdd(out, s);
+}
+
+static constexpr uint32_t kCALog = 12, kCAThreads = 128;   // 4096 slots x 8 B = 32 KB, <= 2048 entries
+static constexpr uint32_t kCBLog = 14, kCBThreads = 256;   // 16384 slots = 128 KB, <= 8192 entries
+
+hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match, uint32_t *gamma,
+                         hgp_csr *C, hgp_nbrs *CN, hgp_level_stats *stats) {
+  hgp_status st = HGP_OK;
+  const uint32_t N = g->N, E = g->E;
+  const uint64_t P = g->P;
+  memset(C, 0, sizeof(*C));
+  memset(CN, 0, sizeof(*CN));
+  HGP_TRY(clear_errors(c));
+  auto grid_for = [&](uint64_t n, uint32_t per = 256) -> uint32_t {
+    uint64_t b = (n + per - 1) / per;
+    uint64_t cap = 16ull * c->sm_count;
+    return (uint32_t)(b < cap ? (b ? b : 1) : cap);
+  };
+  // ---- gamma
+  uint32_t *rep = scratch_raw<uint32_t>(c, N, &st);
+  uint64_t *cid = scratch_raw<uint64_t>(c, (size_t)N + 1, &st);
+  if (st) return st;
+  HGP_TRY(launch(c, "rep", k_rep, dim3(grid_for(N)), dim3(256), 0, match, N, rep, c->d_err));
+  uint64_t Nc64 = 0;
+  HGP_TRY(scan_exclusive(c, InU32{rep}, N, cid, &Nc64));
+  uint64_t err[kErrSlots];
+  HGP_TRY(fetch_errors(c, err));
+  if (err[kErrMatch] != UINT64_MAX)
+    return set_error(HGP_E_ARG, "node %llu: match is not symmetric", (unsigned long long)err[kErrMatch]);
+  const uint32_t Nc = (uint32_t)Nc64;
+  C->N = Nc;
+  C->node_w = dalloc_n<uint32_t>(c, Nc, &st);
+  uint32_t *mem = scratch_raw<uint32_t>(c, 2 * (size_t)Nc, &st);
+  if (st) return st;
+  uint32_t *mem0 = mem, *mem1 = mem + Nc;
+  HGP_CUDA(cudaMemsetAsync(C->node_w, 0, 4 * (size_t)(Nc ? Nc : 1), c->stream));
+  HGP_TRY(launch(c, "gamma", k_gamma, dim3(grid_for(N)), dim3(256), 0, match, (const uint64_t *)cid,
+                 (const uint32_t *)g->node_w, N, gamma, C->node_w, mem0, mem1));
+  // ---- coarse edges in oversized slots
+  uint32_t *x = scratch_raw<uint32_t>(c, P, &st);
+  uint32_t *cnsrc = scratch_raw<uint32_t>(c, E, &st);
+  uint32_t *csize = scratch_raw<uint32_t>(c, E, &st);
+  uint8_t *keep = scratch_raw<uint8_t>(c, E, &st);
+  uint64_t *fp = scratch_raw<uint64_t>(c, E, &st);
+  if (st) return st;
+  HGP_TRY(launch(c, "map_pins", k_map_pins, dim3(grid_for(P)), dim3(256), 0, (const uint32_t *)g->pins,
+                 (const uint32_t *)gamma, P, x));
+  HGP_TRY(segmented_sort(c, EdgeSeg2{g->edge_off, g->edge_nsrc}, 2 * (uint64_t)E, x, g->max_edge));
+  HGP_TRY(launch(c, "edge_unique", k_edge_unique, dim3(grid_for(E, 8)), dim3(256), 0, (const uint64_t *)g->edge_off,
+                 (const uint32_t *)g->edge_nsrc, E, x, cnsrc, csize, keep, fp));
+  // ---- merge parallel edges
+  uint32_t log2t = 4;
+  while ((1ull << log2t) < 2ull * E + 16) ++log2t;
+  MergeJob M{};
+  M.off = g->edge_off; M.x = x; M.cnsrc = cnsrc; M.csize = csize; M.keep = keep; M.fp = fp; M.E = E;
+  M.owner = scratch_raw<uint32_t>(c, (size_t)1 << log2t, &st);
+  M.minrep = scratch_raw<uint32_t>(c, (size_t)1 << log2t, &st);
+  M.slot_of = scratch_raw<uint32_t>(c, E, &st);
+  M.log2t = log2t;
+  uint32_t *erep = scratch_raw<uint32_t>(c, E, &st);
+  uint32_t *is_rep = scratch_raw<uint32_t>(c, E, &st);
+  uint64_t *ceid = scratch_raw<uint64_t>(c, (size_t)E + 1, &st);
+  if (st) return st;
+  HGP_CUDA(cudaMemsetAsync(M.owner, 0xFF, 4ull << log2t, c->stream));
+  HGP_CUDA(cudaMemsetAsync(M.minrep, 0xFF, 4ull << log2t, c->stream));
+  HGP_TRY(launch(c, "merge_insert", k_merge_insert, dim3(grid_for(E)), dim3(256), 0, M));
+  HGP_TRY(launch(c, "merge_resolve", k_merge_resolve, dim3(grid_for(E)), dim3(256), 0, M, erep, is_rep));
+  uint64_t Ec64 = 0;
+  HGP_TRY(scan_exclusive(c, InU32{is_rep}, E, ceid, &Ec64));
+  const uint32_t Ec = (uint32_t)Ec64;
+  C->E = Ec;
+  C->edge_off = dalloc_n<uint64_t>(c, (size_t)Ec + 1, &st);
+  C->edge_nsrc = dalloc_n<uint32_t>(c, Ec, &st);
+  C->edge_w = dalloc_n<uint32_t>(c, Ec, &st);
+  C->edge_mu = dalloc_n<uint32_t>(c, Ec, &st);
+  uint32_t *c_size = scratch_raw<uint32_t>(c, Ec, &st);
+  unsigned int *maxes = scratch_zero<unsigned int>(c, 4, &st);
+  if (st) return st;
+  HGP_CUDA(cudaMemsetAsync(C->edge_w, 0, 4 * (size_t)(Ec ? Ec : 1), c->stream));
+  HGP_CUDA(cudaMemsetAsync(C->edge_mu, 0, 4 * (size_t)(Ec ? Ec : 1), c->stream));
+  HGP_TRY(launch(c, "coarse_edge_attrs", k_coarse_edge_attrs, dim3(grid_for(E)), dim3(256), 0, (const uint32_t *)erep,
+                 (const uint64_t *)ceid, (const uint32_t *)g->edge_w, (const uint32_t *)g->edge_mu,
+                 (const uint32_t *)cnsrc, (const uint32_t *)csize, E, C->edge_w, C->edge_mu, C->edge_nsrc, c_size));
+  uint64_t Pc = 0;
+  HGP_TRY(scan_exclusive(c, InU32{c_size}, Ec, C->edge_off, &Pc));
+  C->P = Pc;
+  C->pins = dalloc_n<uint32_t>(c, Pc, &st);
+  if (st) return st;
+  HGP_TRY(launch(c, "coarse_edge_pack", k_coarse_edge_pack, dim3(grid_for(E, 8)), dim3(256), 0, (const uint32_t *)erep,
+                 (const uint64_t *)ceid, (const uint64_t *)g->edge_off, (const uint32_t *)x, (const uint32_t *)csize,
+                 (const uint64_t *)C->edge_off, E, C->pins, maxes));
+  uint32_t hmax[4];
+  HGP_TRY(read_back(c, maxes, 16, hmax));
+  C->max_edge = hmax[0];
+  HGP_TRY(build_incidence(c, C));
+  // ---- coarse neighbours
+  uint64_t *bound_off = scratch_raw<uint64_t>(c, (size_t)Nc + 1, &st);
+  if (st) return st;
+  uint64_t Vb = 0;
+  HGP_TRY(scan_exclusive(c, BoundIn{mem0, mem1, nb->off}, Nc, bound_off, &Vb));
+  uint32_t *pool = scratch_raw<uint32_t>(c, Vb, &st);
+  uint32_t *ccnt = scratch_raw<uint32_t>(c, Nc, &st);
+  uint32_t *lists = scratch_raw<uint32_t>(c, 2 * (size_t)Nc, &st);
+  uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
+  unsigned long long *misc = scratch_zero<unsigned long long>(c, 2, &st);   // purged, max bound (tier C)
+  if (st) return st;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_coarse_nbrs<kCAThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 << kCALog);
+    cudaFuncSetAttribute(k_coarse_nbrs<kCBThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 << kCBLog);
+    attr = true;
+  }
+  CNbrJob J{};
+  J.mem0 = mem0; J.mem1 = mem1; J.nb_off = nb->off; J.nbr = nb->nbr; J.gamma = gamma; J.bound_off = bound_off;
+  J.pool = pool; J.cnt = ccnt; J.Nc = Nc; J.purged = misc;
+  const uint32_t capA = 1u << (kCALog - 1), capB = 1u << (kCBLog - 1);
+  J.list = nullptr; J.list_count = nullptr; J.cap = capA; J.log2s = kCALog;
+  const uint32_t gA = Nc < 64u * c->sm_count ? (Nc ? Nc : 1) : 64u * c->sm_count;
+  HGP_TRY(launch(c, "coarse_nbrs_A", k_coarse_nbrs<kCAThreads, true>, dim3(gA), dim3(kCAThreads), 8u << kCALog, J));
+  HGP_TRY(launch(c, "cnbr_classify", k_cnbr_classify, dim3(grid_for(Nc)), dim3(256), 0, (const uint64_t *)bound_off, Nc,
+                 capA, capB, lists, lists + Nc, counts, misc + 1));
+  uint32_t hc[2];
+  HGP_TRY(read_back(c, counts, 8, hc));
+  if (hc[0]) {
+    J.list = lists; J.list_count = counts; J.cap = capB; J.log2s = kCBLog;
+    HGP_TRY(launch(c, "coarse_nbrs_B", k_coarse_nbrs<kCBThreads, true>, dim3(c->sm_count), dim3(kCBThreads),
+                   8u << kCBLog, J));
+  }
+  if (hc[1]) {
+    uint64_t mb = 0;
+    HGP_TRY(read_u64(c, (const uint64_t *)(misc + 1), &mb));
+    uint32_t lg = kCBLog;
+    while ((1ull << (lg - 1)) < mb) ++lg;
+    const uint32_t ctas = hc[1] < (uint32_t)c->sm_count ? hc[1] : (uint32_t)c->sm_count;
+    uint32_t *gtab = scratch_raw<uint32_t>(c, (size_t)ctas << (lg + 1), &st);
+    if (st) return st;
+    J.list = lists + Nc; J.list_count = counts + 1; J.cap = 0xFFFFFFFFu; J.log2s = lg; J.gtab = gtab;
+    HGP_TRY(launch(c, "coarse_nbrs_C", k_coarse_nbrs<256, false>, dim3(ctas), dim3(256), 0, J));
+  }
+  CN->lo = 0;
+  CN->hi = Nc;
+  CN->off = dalloc_n<uint64_t>(c, (size_t)Nc + 1, &st);
+  if (st) return st;
+  uint64_t Vc = 0;
+  HGP_TRY(scan_exclusive(c, InU32{ccnt}, Nc, CN->off, &Vc));
+  CN->V = Vc;
+  CN->nbr = dalloc_n<uint32_t>(c, Vc, &st);
+  if (st) return st;
+  HGP_TRY(launch(c, "cnbr_pack", k_cnbr_pack, dim3(grid_for(Nc, 8)), dim3(256), 0, (const uint32_t *)pool,
+                 (const uint64_t *)bound_off, (const uint32_t *)ccnt, (const uint64_t *)CN->off, Nc, CN->nbr, maxes + 1));
+  uint64_t purged = 0;
+  HGP_TRY(read_back(c, maxes, 16, hmax));
+  HGP_TRY(read_u64(c, (const uint64_t *)misc, &purged));
+  CN->max_deg = hmax[1];
+  if (stats) {
+    uint64_t kept = 0;
+    // kept edges = classes' members; dropped = E - kept; merged = kept - Ec
+    uint32_t *kc = scratch_zero<uint32_t>(c, 1, &st);
+    if (st) return st;
+    HGP_TRY(launch(c, "count_kept", k_count_kept, dim3(grid_for(E)), dim3(256), 0, (const uint32_t *)erep, E, kc));
+    uint32_t hk = 0;
+    HGP_TRY(read_back(c, kc, 4, &hk));
+    kept = hk;
+    stats->Nc = Nc; stats->Ec = Ec; stats->Pc = Pc; stats->Vc = Vc;
+    stats->dropped_edges = (uint32_t)(E - kept);
+    stats->merged_edges = (uint32_t)(kept - Ec);
+    stats->purged = purged;
+  }
+  return HGP_OK;
+}
+
+}  // namespace hgp
+
+using namespace hgp;
+
+extern "C" hgp_status hgp_contract(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match,
+                                   uint32_t *gamma, hgp_csr *coarse, hgp_nbrs *coarse_nb) {
+  if (!c || !g || !nb || !match || !gamma || !coarse || !coarse_nb)
+    return set_error(HGP_E_ARG, "hgp_contract: null argument");
+  if (nb->lo != 0 || nb->hi != g->N) return set_error(HGP_E_ARG, "contract needs neighbours of every node");
+  ApiScope scope(c);
+  hgp_status s = contract_impl(c, g, nb, match, gamma, coarse, coarse_nb, nullptr);
+  if (s != HGP_OK) { free_csr(c, coarse); free_nbrs(c, coarse_nb); }
+  return s;
+}

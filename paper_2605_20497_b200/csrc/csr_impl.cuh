@@ -1,0 +1,10 @@
+// csr_impl.cuh — helpers shared by the a1 and a5 translation units of the product library.
+#pragma once
+#include "common.cuh"
+
+namespace hgp {
+// Allocate and fill inc_off / inc_nin / inc / in_mu / max_inc of g from its edge arrays.
+hgp_status build_incidence(hgp_ctx *c, hgp_csr *g);
+void free_csr(hgp_ctx *c, hgp_csr *g);
+void free_nbrs(hgp_ctx *c, hgp_nbrs *nb);
+}  // namespace hgp

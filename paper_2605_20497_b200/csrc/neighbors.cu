@@ -1,0 +1,264 @@
+// neighbors.cu — a2: materialise N(n) = (U_{e in I(n)} e) \ {n}.
+//
+// One CTA per node deduplicates the pins of its incident hyperedges in an open-addressing
+// hash set (shared memory; global memory for giant neighbourhoods), then appends the unique
+// ids to a pool at an atomically reserved offset; a scan of the counts and a pack give the
+// CSR. Segments are sets (hash order), see include/hgp.h.
+#include "csr_impl.cuh"
+#include "hashset.cuh"
+#include "scan.cuh"
+
+namespace hgp {
+
+struct NbrJob {
+  const uint64_t *inc_off;
+  const uint32_t *inc;
+  const uint64_t *edge_off;
+  const uint32_t *pins;
+  uint32_t lo;
+  const uint32_t *list;        // nodes to process (nullptr: lo + t for t < nall)
+  const uint32_t *list_count;  // device count of list (nullptr: nall)
+  uint32_t nall;
+  uint32_t log2s;              // table size
+  uint32_t cap;                // max uniques before declaring overflow
+  uint32_t *gtab;              // global tables (one per CTA) when not in smem
+  uint32_t *pool;
+  uint64_t pool_cap;
+  unsigned long long *pool_cursor;
+  uint64_t *start;             // [hi-lo]
+  uint32_t *cnt;               // [hi-lo]
+  uint32_t *ovf_list, *ovf_count;    // table overflow -> next tier
+  uint32_t *pool_list, *pool_count;  // pool overflow -> rerun after growing the pool
+};
+
+template <int THREADS, bool SMEM>
+__global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
+  extern __shared__ uint32_t dyn[];
+  __shared__ uint32_t s_cnt;
+  __shared__ uint32_t s_state;    // 0 ok, 1 table overflow, 2 pool overflow
+  __shared__ unsigned long long s_start;
+  __shared__ uint64_t wt[33];
+  constexpr uint32_t NW = THREADS / 32;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t S = 1u << J.log2s;
+  uint32_t *tab = SMEM ? dyn : J.gtab + ((size_t)blockIdx.x << J.log2s);
+  const uint32_t total = J.list_count ? *J.list_count : J.nall;
+  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const uint32_t n = J.list ? J.list[t] : J.lo + t;
+    for (uint32_t i = tid; i < S; i += THREADS) tab[i] = kEmpty;
+    if (tid == 0) { s_cnt = 0; s_state = 0; }
+    __syncthreads();
+    const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1];
+    volatile uint32_t *vcnt = &s_cnt;
+    bool stop = false;
+    for (uint64_t k = i0 + w; k < i1 && !stop; k += NW) {
+      const uint32_t e = J.inc[k];
+      const uint64_t a = J.edge_off[e], b = J.edge_off[e + 1];
+      for (uint64_t base = a; base < b; base += 32) {        // warp-uniform trip count
+        // warp-uniform decision: lanes may reach this point at different times (independent
+        // thread scheduling), so vote instead of trusting each lane's own read
+        if (__any_sync(0xFFFFFFFFu, *vcnt >= J.cap)) { stop = true; break; }
+        const uint64_t j = base + lane;
+        if (j < b) {
+          const uint32_t m = J.pins[j];
+          if (m != n && hs_insert(tab, J.log2s, m)) atomicAdd(&s_cnt, 1u);
+        }
+      }
+    }
+    if (stop && lane == 0) s_state = 1;
+    __syncthreads();
+    const uint32_t count = s_cnt;
+    if (s_state == 0 && tid == 0) {
+      unsigned long long st = atomicAdd(J.pool_cursor, (unsigned long long)count);
+      s_start = st;
+      if (st + count > J.pool_cap) s_state = 2;
+    }
+    __syncthreads();
+    if (s_state == 1) {
+      if (tid == 0) J.ovf_list[atomicAdd(J.ovf_count, 1u)] = n;
+    } else if (s_state == 2) {
+      if (tid == 0) J.pool_list[atomicAdd(J.pool_count, 1u)] = n;
+    } else {
+      // compact the table's keys into pool[s_start ...] (thread-contiguous slot ranges)
+      const uint32_t per = S / THREADS;
+      const uint32_t base = tid * per;
+      uint64_t mine = 0;
+      for (uint32_t i = 0; i < per; ++i) mine += tab[base + i] != kEmpty;
+      uint64_t tot;
+      uint64_t pos = s_start + block_excl_scan<uint64_t>(mine, wt, &tot);
+      for (uint32_t i = 0; i < per; ++i) {
+        const uint32_t k = tab[base + i];
+        if (k != kEmpty) J.pool[pos++] = k;
+      }
+      if (tid == 0) { J.start[n - J.lo] = s_start; J.cnt[n - J.lo] = count; }
+    }
+    __syncthreads();
+  }
+}
+
+// bound_n = min(N-1, sum_{e in I(n)} (|e|-1)) for the listed nodes -> atomicMax
+__global__ void k_nbr_bound(const uint64_t *inc_off, const uint32_t *inc, const uint64_t *edge_off,
+                            const uint32_t *list, const uint32_t *count, uint32_t N, unsigned long long *mx) {
+  const uint32_t total = *count;
+  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < total; t += gridDim.x * (blockDim.x >> 5)) {
+    const uint32_t n = list[t];
+    uint64_t s = 0;
+    for (uint64_t k = inc_off[n] + lane_id(); k < inc_off[n + 1]; k += 32) {
+      const uint32_t e = inc[k];
+      s += edge_off[e + 1] - edge_off[e] - 1;
+    }
+    s = warp_sum(s);
+    if (s > N - 1) s = N - 1;
+    if (lane_id() == 0) atomicMax(mx, (unsigned long long)s);
+  }
+}
+
+__global__ void k_nbr_pack(const uint32_t *pool, const uint64_t *start, const uint32_t *cnt, const uint64_t *off,
+                           uint32_t nn, uint32_t *nbr, unsigned int *maxdeg) {
+  const uint32_t lane = lane_id();
+  uint32_t mx = 0;
+  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < nn; t += gridDim.x * (blockDim.x >> 5)) {
+    const uint32_t c = cnt[t];
+    const uint32_t *src = pool + start[t];
+    uint32_t *dst = nbr + off[t];
+    for (uint32_t j = lane; j < c; j += 32) dst[j] = src[j];
+    mx = max(mx, c);
+  }
+  mx = warp_max(mx);
+  if (lane == 0) atomicMax(maxdeg, mx);
+}
+
+__global__ void k_edge_pairs(const uint64_t *edge_off, uint32_t E, unsigned long long *T) {
+  uint64_t s = 0;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const uint64_t d = edge_off[e + 1] - edge_off[e];
+    s += d * (d - 1);
+  }
+  s = warp_sum(s);
+  if (lane_id() == 0) atomicAdd(T, (unsigned long long)s);
+}
+
+void free_nbrs(hgp_ctx *c, hgp_nbrs *nb) {
+  if (!nb) return;
+  c->dfree(nb->off, 8 * ((size_t)(nb->hi - nb->lo) + 1));
+  c->dfree(nb->nbr, 4 * nb->V);
+  memset(nb, 0, sizeof(*nb));
+}
+
+static constexpr uint32_t kT1Log = 12, kT1Threads = 128;   // 16 KB table, <= 1920 uniques
+static constexpr uint32_t kT2Log = 15, kT2Threads = 256;   // 128 KB table
+
+}  // namespace hgp
+
+using namespace hgp;
+
+extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_t lo, uint32_t hi, hgp_nbrs *out) {
+  if (!c || !g || !out || lo > hi || hi > g->N) return set_error(HGP_E_ARG, "hgp_unique_neighbors: bad argument");
+  ApiScope scope(c);
+  memset(out, 0, sizeof(*out));
+  hgp_status st = HGP_OK;
+  const uint32_t nn = hi - lo;
+  out->lo = lo;
+  out->hi = hi;
+  out->off = dalloc_n<uint64_t>(c, (size_t)nn + 1, &st);
+  if (st) return st;
+  if (nn == 0) {
+    HGP_CUDA(cudaMemsetAsync(out->off, 0, 8, c->stream));
+    out->nbr = dalloc_n<uint32_t>(c, 1, &st);
+    return st;
+  }
+  // pool capacity: min(T, 24 P + nn) with T = sum_e |e|(|e|-1) >= total pre-dedup candidates
+  unsigned long long *misc = scratch_zero<unsigned long long>(c, 4, &st);   // T, cursor, bound, -
+  uint32_t *counters = scratch_zero<uint32_t>(c, 8, &st);                  // ovf1, ovf2, poolovf, maxdeg
+  uint64_t *start = scratch_raw<uint64_t>(c, nn, &st);
+  uint32_t *cnt = scratch_raw<uint32_t>(c, nn, &st);
+  uint32_t *list1 = scratch_raw<uint32_t>(c, nn, &st);
+  uint32_t *list2 = scratch_raw<uint32_t>(c, nn, &st);
+  uint32_t *plist = scratch_raw<uint32_t>(c, nn, &st);
+  if (st) return st;
+  HGP_TRY(launch(c, "edge_pairs", k_edge_pairs, dim3(g->E ? (div_up(g->E, 256) < 1024 ? div_up(g->E, 256) : 1024) : 0),
+                 dim3(256), 0, (const uint64_t *)g->edge_off, g->E, misc));
+  uint64_t T = 0;
+  HGP_TRY(read_u64(c, (const uint64_t *)misc, &T));
+  uint64_t pool_cap = T < 24 * g->P + nn ? T : 24 * g->P + nn;
+  if (pool_cap == 0) pool_cap = 1;
+  uint32_t *pool = scratch_raw<uint32_t>(c, pool_cap, &st);
+  if (st) return st;
+
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_nbrs<kT1Threads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT1Log);
+    cudaFuncSetAttribute(k_nbrs<kT2Threads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT2Log);
+    attr = true;
+  }
+  // Run the three tiers with a given pool; returns pool-overflow count and the pool cursor
+  // (= exact total of unique entries once every node has deduplicated).
+  auto run_tiers = [&](uint32_t *pool, uint64_t pool_cap, uint32_t *n_pool_ovf, uint64_t *cursor) -> hgp_status {
+    HGP_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(uint32_t), c->stream));
+    HGP_CUDA(cudaMemsetAsync(misc + 1, 0, 3 * sizeof(unsigned long long), c->stream));
+    NbrJob J{};
+    J.inc_off = g->inc_off; J.inc = g->inc; J.edge_off = g->edge_off; J.pins = g->pins;
+    J.lo = lo; J.pool = pool; J.pool_cap = pool_cap; J.pool_cursor = misc + 1;
+    J.start = start; J.cnt = cnt; J.pool_list = plist; J.pool_count = counters + 2;
+    // tier 1: every node, 16 KB shared table
+    J.list = nullptr; J.list_count = nullptr; J.nall = nn;
+    J.log2s = kT1Log; J.cap = (1u << (kT1Log - 1)) - 32 * (kT1Threads / 32);
+    J.ovf_list = list1; J.ovf_count = counters + 0;
+    const uint32_t grid1 = nn < 32u * c->sm_count ? nn : 32u * c->sm_count;
+    HGP_TRY(launch(c, "nbrs_t1", k_nbrs<kT1Threads, true>, dim3(grid1), dim3(kT1Threads), 4u << kT1Log, J));
+    // tier 2: 128 KB shared table for the overflowed nodes (grid-stride over a device count)
+    J.list = list1; J.list_count = counters + 0;
+    J.log2s = kT2Log; J.cap = (1u << (kT2Log - 1)) - 32 * (kT2Threads / 32);
+    J.ovf_list = list2; J.ovf_count = counters + 1;
+    HGP_TRY(launch(c, "nbrs_t2", k_nbrs<kT2Threads, true>, dim3(c->sm_count), dim3(kT2Threads), 4u << kT2Log, J));
+    uint32_t hc[4];
+    HGP_TRY(read_back(c, counters, 16, hc));
+    if (hc[1]) {   // tier 3: global-memory tables sized from the neighbourhood bound
+      HGP_TRY(launch(c, "nbr_bound", k_nbr_bound, dim3(c->sm_count), dim3(256), 0, (const uint64_t *)g->inc_off,
+                     (const uint32_t *)g->inc, (const uint64_t *)g->edge_off, (const uint32_t *)list2,
+                     (const uint32_t *)(counters + 1), g->N, misc + 2));
+      uint64_t mb = 0;
+      HGP_TRY(read_u64(c, (const uint64_t *)(misc + 2), &mb));
+      uint32_t lg = 1;
+      while ((1ull << lg) < 2 * (mb + 1) + 32 * 8) ++lg;
+      const uint32_t ctas = hc[1] < (uint32_t)c->sm_count ? hc[1] : (uint32_t)c->sm_count;
+      uint32_t *gtab = scratch_raw<uint32_t>(c, (size_t)ctas << lg, &st);
+      if (st) return st;
+      J.list = list2; J.list_count = counters + 1; J.log2s = lg; J.cap = 0xFFFFFFFFu; J.gtab = gtab;
+      J.ovf_list = list1; J.ovf_count = counters + 4;   // cannot overflow: table >= 2 (bound + 1)
+      HGP_TRY(launch(c, "nbrs_t3", k_nbrs<256, false>, dim3(ctas), dim3(256), 0, J));
+      HGP_TRY(read_back(c, counters, 16, hc));
+    }
+    *n_pool_ovf = hc[2];
+    return read_u64(c, (const uint64_t *)(misc + 1), cursor);
+  };
+  uint32_t n_pool_ovf = 0;
+  uint64_t cursor = 0;
+  HGP_TRY(run_tiers(pool, pool_cap, &n_pool_ovf, &cursor));
+  for (int attempt = 0; n_pool_ovf; ++attempt) {   // estimate too short: the cursor holds the exact total
+    if (attempt == 2) return set_error(HGP_E_INTERNAL, "hgp_unique_neighbors: pool sizing failed");
+    pool_cap = cursor;
+    pool = scratch_raw<uint32_t>(c, pool_cap, &st);
+    if (st) return st;
+    HGP_TRY(run_tiers(pool, pool_cap, &n_pool_ovf, &cursor));
+  }
+  uint64_t V = 0;
+  HGP_TRY(scan_exclusive(c, InU32{cnt}, nn, out->off, &V));
+  out->V = V;
+  out->nbr = dalloc_n<uint32_t>(c, V, &st);
+  if (st) { free_nbrs(c, out); return st; }
+  unsigned int *d_max = counters + 3;
+  hgp_status s = launch(c, "nbr_pack", k_nbr_pack, dim3(nn / 8 + 1 < 16u * c->sm_count ? nn / 8 + 1 : 16u * c->sm_count),
+                        dim3(256), 0, (const uint32_t *)pool, (const uint64_t *)start, (const uint32_t *)cnt,
+                        (const uint64_t *)out->off, nn, out->nbr, d_max);
+  if (s) { free_nbrs(c, out); return s; }
+  uint32_t mx = 0;
+  s = read_back(c, d_max, 4, &mx);
+  if (s) { free_nbrs(c, out); return s; }
+  out->max_deg = mx;
+  return HGP_OK;
+}
+
+extern "C" void hgp_nbrs_free(hgp_ctx *c, hgp_nbrs *nb) {
+  if (c && nb) free_nbrs(c, nb);
+}
