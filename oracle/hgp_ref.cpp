@@ -255,7 +255,8 @@ int hgp_ref_score_pairs(const hgp_ref_csr *g, hgp_ref_nbrs *nb, const hgp_ref_pa
   auto noise = [&](uint32_t n, uint32_t m) -> uint64_t {          // rng(min(n,m), max(n,m))
     if (p->noise_cap == 0) return 0;
     uint64_t key = (static_cast<uint64_t>(std::min(n, m)) << 32) | std::max(n, m);
-    return splitmix64(key ^ seed_mix) % (p->noise_cap + 1);
+    // uniform in [0, cap]: floor(hash * (cap + 1) / 2^64) (reading #3)
+    return static_cast<uint64_t>(((unsigned __int128)splitmix64(key ^ seed_mix) * (p->noise_cap + 1)) >> 64);
   };
   struct Bin { uint32_t id; uint64_t pos; uint64_t eta; uint64_t inter; };
   for (uint32_t n = nb->lo; n < nb->hi; ++n) {

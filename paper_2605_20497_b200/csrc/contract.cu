@@ -222,14 +222,36 @@ struct CNbrJob {
   unsigned long long *purged;
 };
 
+// insert key with an OR-ed flag kept in bit 31 of the slot (ids < 2^31 - 1, kEmpty masks to
+// 0x7FFFFFFF which is never an id); returns true if this call inserted the key.
+__device__ __forceinline__ bool hs_insert_flagged(uint32_t *keys, uint32_t log2s, uint32_t key, bool flag,
+                                                  uint32_t *slot_out) {
+  const uint32_t mask = (1u << log2s) - 1;
+  uint32_t s = hash_slot(key, log2s);
+  volatile uint32_t *vk = keys;
+  while (true) {
+    uint32_t k = vk[s];
+    if (k == kEmpty) {
+      k = atomicCAS(&keys[s], kEmpty, flag ? (key | kPurge) : key);
+      if (k == kEmpty) { *slot_out = s; return true; }
+    }
+    if ((k & kIdMask) == key) {
+      if (flag && !(k & kPurge)) atomicOr(&keys[s], kPurge);
+      *slot_out = s;
+      return false;
+    }
+    s = (s + 1) & mask;
+  }
+}
+
 template <int THREADS, bool SMEM>
 __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
   extern __shared__ uint32_t dyn[];
-  __shared__ uint64_t wt[33];
+  __shared__ uint32_t s_cnt, s_out;
   const uint32_t tid = threadIdx.x;
   const uint32_t S = 1u << J.log2s;
-  uint32_t *keys = SMEM ? dyn : J.gtab + ((size_t)blockIdx.x << (J.log2s + 1));
-  uint32_t *flag = keys + S;
+  uint32_t *keys = SMEM ? dyn : J.gtab + (size_t)blockIdx.x * (((size_t)3 << J.log2s) >> 1);
+  uint32_t *slots = keys + S;                                       // append list of inserted slots
   const uint32_t total = J.list_count ? *J.list_count : J.Nc;
   uint64_t purged = 0;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
@@ -239,30 +261,39 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
     const uint64_t b0 = b == kNone ? 0 : J.nb_off[b], b1 = b == kNone ? 0 : J.nb_off[b + 1];
     const uint64_t na = a1 - a0, nbn = b1 - b0;
     if (!J.list && na + nbn > J.cap) continue;                      // larger tier (uniform)
-    for (uint32_t i = tid; i < S; i += THREADS) { keys[i] = kEmpty; flag[i] = 0; }
+    for (uint32_t i = tid; i < S / 4; i += THREADS)
+      reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    if (tid == 0) { s_cnt = 0; s_out = 0; }
     __syncthreads();
-    for (uint64_t k = tid; k < na + nbn; k += THREADS) {
-      const uint32_t v = k < na ? J.nbr[a0 + k] : J.nbr[b0 + (k - na)];
-      const uint32_t gm = J.gamma[v & kIdMask];
-      bool ins;
-      const uint32_t slot = hs_insert_slot(keys, J.log2s, gm, &ins);
-      if (v & kPurge) { flag[slot] = 1; ++purged; }
+    // 4 entries per thread in flight: nbr loads, then the gamma gathers, then the inserts
+    for (uint64_t k0 = tid; k0 < na + nbn; k0 += 4 * THREADS) {
+      uint32_t v[4], gm[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint64_t k = k0 + (uint64_t)u * THREADS;
+        v[u] = k < na + nbn ? (k < na ? J.nbr[a0 + k] : J.nbr[b0 + (k - na)]) : kEmpty;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) gm[u] = v[u] != kEmpty ? __ldg(J.gamma + (v[u] & kIdMask)) : kEmpty;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (v[u] == kEmpty) continue;
+        uint32_t slot;
+        const bool fl = (v[u] & kPurge) != 0;
+        if (hs_insert_flagged(keys, J.log2s, gm[u], fl, &slot)) slots[atomicAdd(&s_cnt, 1u)] = slot;
+        purged += fl;
+      }
     }
     __syncthreads();
-    const uint32_t per = S / THREADS, base = tid * per;
-    uint64_t mine = 0;
-    for (uint32_t i = 0; i < per; ++i) {
-      const uint32_t k = keys[base + i];
-      mine += k != kEmpty && k != c && !flag[base + i];
+    const uint32_t nk = s_cnt;
+    uint64_t *dummy = nullptr;
+    (void)dummy;
+    for (uint32_t i = tid; i < nk; i += THREADS) {
+      const uint32_t k = keys[slots[i]];
+      if (!(k & kPurge) && k != c) J.pool[J.bound_off[c] + atomicAdd(&s_out, 1u)] = k;
     }
-    uint64_t tot;
-    uint64_t pos = J.bound_off[c] + block_excl_scan<uint64_t>(mine, wt, &tot);
-    for (uint32_t i = 0; i < per; ++i) {
-      const uint32_t k = keys[base + i];
-      if (k != kEmpty && k != c && !flag[base + i]) J.pool[pos++] = k;
-    }
-    if (tid == 0) J.cnt[c] = (uint32_t)tot;
     __syncthreads();
+    if (tid == 0) J.cnt[c] = s_out;
   }
   purged = warp_sum(purged);
   if ((tid & 31) == 0 && purged) atomicAdd(J.purged, (unsigned long long)purged);
@@ -313,8 +344,8 @@ __global__ void k_count_kept(const uint32_t *rep, uint32_t E, uint32_t *out) {
   if (lane_id() == 0 && s) atomicAdd(out, s);
 }
 
-static constexpr uint32_t kCALog = 12, kCAThreads = 128;   // 4096 slots x 8 B = 32 KB, <= 2048 entries
-static constexpr uint32_t kCBLog = 14, kCBThreads = 256;   // 16384 slots = 128 KB, <= 8192 entries
+static constexpr uint32_t kCALog = 12, kCAThreads = 128;   // 4096 slots + list: 24 KB, <= 2048 entries
+static constexpr uint32_t kCBLog = 15, kCBThreads = 256;   // 32768 slots + list: 192 KB, <= 16384 entries
 
 hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match, uint32_t *gamma,
                          hgp_csr *C, hgp_nbrs *CN, hgp_level_stats *stats) {
@@ -419,8 +450,8 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   if (st) return st;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_coarse_nbrs<kCAThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 << kCALog);
-    cudaFuncSetAttribute(k_coarse_nbrs<kCBThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 << kCBLog);
+    cudaFuncSetAttribute(k_coarse_nbrs<kCAThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 << kCALog);
+    cudaFuncSetAttribute(k_coarse_nbrs<kCBThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 << kCBLog);
     attr = true;
   }
   CNbrJob J{};
@@ -429,7 +460,7 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   const uint32_t capA = 1u << (kCALog - 1), capB = 1u << (kCBLog - 1);
   J.list = nullptr; J.list_count = nullptr; J.cap = capA; J.log2s = kCALog;
   const uint32_t gA = Nc < 64u * c->sm_count ? (Nc ? Nc : 1) : 64u * c->sm_count;
-  HGP_TRY(launch(c, "coarse_nbrs_A", k_coarse_nbrs<kCAThreads, true>, dim3(gA), dim3(kCAThreads), 8u << kCALog, J));
+  HGP_TRY(launch(c, "coarse_nbrs_A", k_coarse_nbrs<kCAThreads, true>, dim3(gA), dim3(kCAThreads), 6u << kCALog, J));
   HGP_TRY(launch(c, "cnbr_classify", k_cnbr_classify, dim3(grid_for(Nc)), dim3(256), 0, (const uint64_t *)bound_off, Nc,
                  capA, capB, lists, lists + Nc, counts, misc + 1));
   uint32_t hc[2];
@@ -437,7 +468,7 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   if (hc[0]) {
     J.list = lists; J.list_count = counts; J.cap = capB; J.log2s = kCBLog;
     HGP_TRY(launch(c, "coarse_nbrs_B", k_coarse_nbrs<kCBThreads, true>, dim3(c->sm_count), dim3(kCBThreads),
-                   8u << kCBLog, J));
+                   6u << kCBLog, J));
   }
   if (hc[1]) {
     uint64_t mb = 0;
@@ -445,7 +476,7 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
     uint32_t lg = kCBLog;
     while ((1ull << (lg - 1)) < mb) ++lg;
     const uint32_t ctas = hc[1] < (uint32_t)c->sm_count ? hc[1] : (uint32_t)c->sm_count;
-    uint32_t *gtab = scratch_raw<uint32_t>(c, (size_t)ctas << (lg + 1), &st);
+    uint32_t *gtab = scratch_raw<uint32_t>(c, ((size_t)ctas * 3 << lg) / 2, &st);
     if (st) return st;
     J.list = lists + Nc; J.list_count = counts + 1; J.cap = 0xFFFFFFFFu; J.log2s = lg; J.gtab = gtab;
     HGP_TRY(launch(c, "coarse_nbrs_C", k_coarse_nbrs<256, false>, dim3(ctas), dim3(256), 0, J));

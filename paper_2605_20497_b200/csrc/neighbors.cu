@@ -37,31 +37,51 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
   __shared__ uint32_t s_cnt;
   __shared__ uint32_t s_state;    // 0 ok, 1 table overflow, 2 pool overflow
   __shared__ unsigned long long s_start;
-  __shared__ uint64_t wt[33];
   constexpr uint32_t NW = THREADS / 32;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t S = 1u << J.log2s;
-  uint32_t *tab = SMEM ? dyn : J.gtab + ((size_t)blockIdx.x << J.log2s);
+  // table of S slots followed by the append list of inserted keys (<= S/2 by the cap)
+  uint32_t *tab = SMEM ? dyn : J.gtab + (size_t)blockIdx.x * (((size_t)3 << J.log2s) >> 1);
+  uint32_t *ulist = tab + S;
   const uint32_t total = J.list_count ? *J.list_count : J.nall;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = J.list ? J.list[t] : J.lo + t;
-    for (uint32_t i = tid; i < S; i += THREADS) tab[i] = kEmpty;
+    for (uint32_t i = tid; i < S / 4; i += THREADS)
+      reinterpret_cast<uint4 *>(tab)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     if (tid == 0) { s_cnt = 0; s_state = 0; }
     __syncthreads();
     const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1];
     volatile uint32_t *vcnt = &s_cnt;
     bool stop = false;
-    for (uint64_t k = i0 + w; k < i1 && !stop; k += NW) {
-      const uint32_t e = J.inc[k];
-      const uint64_t a = J.edge_off[e], b = J.edge_off[e + 1];
-      for (uint64_t base = a; base < b; base += 32) {        // warp-uniform trip count
-        // warp-uniform decision: lanes may reach this point at different times (independent
-        // thread scheduling), so vote instead of trusting each lane's own read
-        if (__any_sync(0xFFFFFFFFu, *vcnt >= J.cap)) { stop = true; break; }
-        const uint64_t j = base + lane;
-        if (j < b) {
-          const uint32_t m = J.pins[j];
-          if (m != n && hs_insert(tab, J.log2s, m)) atomicAdd(&s_cnt, 1u);
+    // a warp loads the offsets of 32 incident edges at once (lane = edge), then walks them with
+    // 128 pins in flight per iteration (4 per lane)
+    for (uint64_t kb = i0 + w; kb < i1 && !stop; kb += (uint64_t)NW * 32) {   // round-robin over warps
+      const uint64_t k = kb + (uint64_t)NW * lane;
+      uint64_t a = 0;
+      uint32_t len = 0;
+      if (k < i1) {
+        const uint32_t e = J.inc[k];
+        a = J.edge_off[e];
+        len = (uint32_t)(J.edge_off[e + 1] - a);
+      }
+      const uint32_t cnt = (uint32_t)min((uint64_t)32, (i1 - kb + NW - 1) / NW);
+      for (uint32_t j = 0; j < cnt && !stop; ++j) {
+        const uint64_t aj = __shfl_sync(0xFFFFFFFFu, a, j);
+        const uint32_t lj = __shfl_sync(0xFFFFFFFFu, len, j);
+        const uint32_t *pj = J.pins + aj;
+        for (uint32_t b4 = 0; b4 < lj; b4 += 128) {
+          // warp-uniform decision: lanes may reach this point at different times (independent
+          // thread scheduling), so vote instead of trusting each lane's own read
+          if (__any_sync(0xFFFFFFFFu, *vcnt >= J.cap)) { stop = true; break; }
+          uint32_t m[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t idx = b4 + u * 32 + lane;
+            m[u] = idx < lj ? __ldg(pj + idx) : n;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (m[u] != n && hs_insert(tab, J.log2s, m[u])) ulist[atomicAdd(&s_cnt, 1u)] = m[u];
         }
       }
     }
@@ -79,17 +99,7 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
     } else if (s_state == 2) {
       if (tid == 0) J.pool_list[atomicAdd(J.pool_count, 1u)] = n;
     } else {
-      // compact the table's keys into pool[s_start ...] (thread-contiguous slot ranges)
-      const uint32_t per = S / THREADS;
-      const uint32_t base = tid * per;
-      uint64_t mine = 0;
-      for (uint32_t i = 0; i < per; ++i) mine += tab[base + i] != kEmpty;
-      uint64_t tot;
-      uint64_t pos = s_start + block_excl_scan<uint64_t>(mine, wt, &tot);
-      for (uint32_t i = 0; i < per; ++i) {
-        const uint32_t k = tab[base + i];
-        if (k != kEmpty) J.pool[pos++] = k;
-      }
+      for (uint32_t i = tid; i < count; i += THREADS) J.pool[s_start + i] = ulist[i];   // coalesced
       if (tid == 0) { J.start[n - J.lo] = s_start; J.cnt[n - J.lo] = count; }
     }
     __syncthreads();
@@ -145,8 +155,8 @@ void free_nbrs(hgp_ctx *c, hgp_nbrs *nb) {
   memset(nb, 0, sizeof(*nb));
 }
 
-static constexpr uint32_t kT1Log = 12, kT1Threads = 128;   // 16 KB table, <= 1920 uniques
-static constexpr uint32_t kT2Log = 15, kT2Threads = 256;   // 128 KB table
+static constexpr uint32_t kT1Log = 12, kT1Threads = 128;   // 16 KB table + 8 KB list, <= 1536 uniques
+static constexpr uint32_t kT2Log = 15, kT2Threads = 256;   // 128 KB table + 64 KB list
 
 }  // namespace hgp
 
@@ -187,8 +197,8 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
 
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_nbrs<kT1Threads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT1Log);
-    cudaFuncSetAttribute(k_nbrs<kT2Threads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT2Log);
+    cudaFuncSetAttribute(k_nbrs<kT1Threads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 << kT1Log);
+    cudaFuncSetAttribute(k_nbrs<kT2Threads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 << kT2Log);
     attr = true;
   }
   // Run the three tiers with a given pool; returns pool-overflow count and the pool cursor
@@ -202,15 +212,15 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
     J.start = start; J.cnt = cnt; J.pool_list = plist; J.pool_count = counters + 2;
     // tier 1: every node, 16 KB shared table
     J.list = nullptr; J.list_count = nullptr; J.nall = nn;
-    J.log2s = kT1Log; J.cap = (1u << (kT1Log - 1)) - 32 * (kT1Threads / 32);
+    J.log2s = kT1Log; J.cap = (1u << (kT1Log - 1)) - 128 * (kT1Threads / 32);
     J.ovf_list = list1; J.ovf_count = counters + 0;
     const uint32_t grid1 = nn < 32u * c->sm_count ? nn : 32u * c->sm_count;
-    HGP_TRY(launch(c, "nbrs_t1", k_nbrs<kT1Threads, true>, dim3(grid1), dim3(kT1Threads), 4u << kT1Log, J));
+    HGP_TRY(launch(c, "nbrs_t1", k_nbrs<kT1Threads, true>, dim3(grid1), dim3(kT1Threads), 6u << kT1Log, J));
     // tier 2: 128 KB shared table for the overflowed nodes (grid-stride over a device count)
     J.list = list1; J.list_count = counters + 0;
-    J.log2s = kT2Log; J.cap = (1u << (kT2Log - 1)) - 32 * (kT2Threads / 32);
+    J.log2s = kT2Log; J.cap = (1u << (kT2Log - 1)) - 128 * (kT2Threads / 32);
     J.ovf_list = list2; J.ovf_count = counters + 1;
-    HGP_TRY(launch(c, "nbrs_t2", k_nbrs<kT2Threads, true>, dim3(c->sm_count), dim3(kT2Threads), 4u << kT2Log, J));
+    HGP_TRY(launch(c, "nbrs_t2", k_nbrs<kT2Threads, true>, dim3(c->sm_count), dim3(kT2Threads), 6u << kT2Log, J));
     uint32_t hc[4];
     HGP_TRY(read_back(c, counters, 16, hc));
     if (hc[1]) {   // tier 3: global-memory tables sized from the neighbourhood bound
@@ -220,9 +230,9 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
       uint64_t mb = 0;
       HGP_TRY(read_u64(c, (const uint64_t *)(misc + 2), &mb));
       uint32_t lg = 1;
-      while ((1ull << lg) < 2 * (mb + 1) + 32 * 8) ++lg;
+      while ((1ull << lg) < 2 * (mb + 1) + 128 * 8) ++lg;
       const uint32_t ctas = hc[1] < (uint32_t)c->sm_count ? hc[1] : (uint32_t)c->sm_count;
-      uint32_t *gtab = scratch_raw<uint32_t>(c, (size_t)ctas << lg, &st);
+      uint32_t *gtab = scratch_raw<uint32_t>(c, ((size_t)ctas * 3 << lg) / 2, &st);
       if (st) return st;
       J.list = list2; J.list_count = counters + 1; J.log2s = lg; J.cap = 0xFFFFFFFFu; J.gtab = gtab;
       J.ovf_list = list1; J.ovf_count = counters + 4;   // cannot overflow: table >= 2 (bound + 1)

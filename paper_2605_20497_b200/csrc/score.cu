@@ -29,16 +29,21 @@ struct ScoreJob {
   uint32_t pi, norm;
   hgp_cand *cand;
   // scheduling
-  const uint32_t *list;        // nodes (nullptr: all of [lo,hi) with degree <= max_deg_here)
+  const uint32_t *list;        // nodes of this launch (nullptr: every node of [lo,hi))
   const uint32_t *list_count;
-  uint32_t max_deg_here;       // tier capacity in neighbour entries
+  uint32_t cap;                // neighbour entries this tier holds (table load <= 1/2)
   uint32_t log2s;
-  uint32_t *gtab;              // global tables when !SMEM: per CTA (4 + 8 + 4) << log2s bytes
+  uint32_t *gtab;              // global tables when !SMEM
+  uint32_t *big_list, *big_count;    // deferred: neighbourhood larger than cap
+  uint32_t *wide_list, *wide_count;  // deferred: packed 32-bit accumulator would overflow
 };
 
+enum { kModeP32 = 0, kModeWide = 1 };
+
+template <int PIMAX>
 struct Top {   // best-first list of (score, id); empty entries have id == kNone
-  uint64_t s[HGP_MAX_PI];
-  uint32_t id[HGP_MAX_PI];
+  uint64_t s[PIMAX];
+  uint32_t id[PIMAX];
 };
 
 __device__ __forceinline__ bool better(uint64_t s1, uint32_t i1, uint64_t s2, uint32_t i2) {
@@ -48,9 +53,10 @@ __device__ __forceinline__ bool better(uint64_t s1, uint32_t i1, uint64_t s2, ui
   return s1 > s2 || (s1 == s2 && i1 > i2);
 }
 
-__device__ __forceinline__ void top_insert(Top &t, uint32_t pi, uint64_t s, uint32_t id) {
+template <int PIMAX>
+__device__ __forceinline__ void top_insert(Top<PIMAX> &t, uint32_t pi, uint64_t s, uint32_t id) {
 #pragma unroll
-  for (int i = 0; i < HGP_MAX_PI; ++i) {
+  for (int i = 0; i < PIMAX; ++i) {
     if (i < (int)pi && better(s, id, t.s[i], t.id[i])) {
       uint64_t ts = t.s[i]; uint32_t ti = t.id[i];
       t.s[i] = s; t.id[i] = id;
@@ -59,111 +65,252 @@ __device__ __forceinline__ void top_insert(Top &t, uint32_t pi, uint64_t s, uint
   }
 }
 
-template <int THREADS, bool SMEM>
+// pi rounds: warp argmax of the lanes' list heads; the winner lane pops its head. Lane 0 writes
+// the merged best-first list to out_s/out_id[0..pi).
+template <int PIMAX>
+__device__ __forceinline__ void warp_top_merge(const Top<PIMAX> &top, uint32_t pi, uint64_t *out_s, uint32_t *out_id) {
+  const uint32_t lane = lane_id();
+  uint32_t head = 0;
+  for (uint32_t r = 0; r < pi; ++r) {
+    uint64_t hs = 0;
+    uint32_t hid = kNone;
+#pragma unroll
+    for (int i = 0; i < PIMAX; ++i)
+      if (i == (int)head) { hs = top.s[i]; hid = top.id[i]; }
+    uint32_t who = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t os = __shfl_xor_sync(0xFFFFFFFFu, hs, o);
+      const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, hid, o);
+      const uint32_t ow = __shfl_xor_sync(0xFFFFFFFFu, who, o);
+      if (better(os, oi, hs, hid)) { hs = os; hid = oi; who = ow; }
+    }
+    if (lane == 0) { out_s[r] = hs; out_id[r] = hid; }
+    if (hid != kNone && who == lane) ++head;
+  }
+}
+
+__device__ __forceinline__ uint64_t gcd64(uint64_t a, uint64_t b) {
+  if (a == 0) return b;
+  if (b == 0) return a;
+  const int sh = __ffsll((long long)(a | b)) - 1;
+  a >>= __ffsll((long long)a) - 1;
+  do {
+    b >>= __ffsll((long long)b) - 1;
+    if (a > b) { uint64_t t = a; a = b; b = t; }
+    b -= a;
+  } while (b);
+  return a << sh;
+}
+
+__device__ __forceinline__ uint64_t edge_c(const ScoreJob &J, uint32_t e, uint64_t a, uint64_t b) {
+  const uint64_t we = (uint64_t)J.edge_w[e] << HGP_FP_SHIFT;   // Eq.5 term, 2^-24 fixed point
+  return J.norm ? we : we / (b - a);
+}
+
+// One CTA per node. MODE kModeP32: one u32 per bin packs (eta/g) << ib | inter, where g is the
+// gcd of the node's c(e) and ib = bits(in_mu(n)) (exact: inter <= in_mu(n) < 2^ib, and the
+// node qualifies only if (sum c / g + 1) << ib <= 2^32); a single native shared-memory atomic
+// add per pin visit. MODE kModeWide: u64 eta + u32 inter per bin.
+template <int THREADS, int MODE, bool SMEM, int PIMAX>
 __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
   extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ uint64_t red_s[THREADS / 32];
-  __shared__ uint32_t red_i[THREADS / 32], red_t[THREADS / 32];
-  __shared__ uint32_t s_win;
+  __shared__ uint64_t s_tops[(THREADS / 32 + 1) * PIMAX];
+  __shared__ uint32_t s_topi[(THREADS / 32 + 1) * PIMAX];
+  __shared__ uint64_t s_sum[THREADS / 32], s_g[THREADS / 32];
+  __shared__ uint32_t s_defer;
+  __shared__ uint64_t s_gcd;
+  __shared__ uint32_t s_ib;
   constexpr uint32_t NW = THREADS / 32;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t log2s = J.log2s, S = 1u << log2s;
-  unsigned char *base = SMEM ? dyn : reinterpret_cast<unsigned char *>(J.gtab) + ((size_t)blockIdx.x * 16 << log2s);
-  uint64_t *eta = reinterpret_cast<uint64_t *>(base);
-  uint32_t *keys = reinterpret_cast<uint32_t *>(base + ((size_t)8 << log2s));
-  uint32_t *inter = reinterpret_cast<uint32_t *>(base + ((size_t)12 << log2s));
+  constexpr uint32_t SLOT = MODE == kModeP32 ? 8 : 16;
+  unsigned char *base = SMEM ? dyn : reinterpret_cast<unsigned char *>(J.gtab) + ((size_t)blockIdx.x * SLOT << log2s);
+  uint32_t *keys = reinterpret_cast<uint32_t *>(base);
+  uint32_t *acc = reinterpret_cast<uint32_t *>(base + ((size_t)4 << log2s));        // P32 acc / wide inter
+  uint64_t *eta = reinterpret_cast<uint64_t *>(base + ((size_t)8 << log2s));        // wide only
   const uint32_t total = J.list_count ? *J.list_count : J.hi - J.lo;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = J.list ? J.list[t] : J.lo + t;
     const uint64_t b0 = J.nb_off[n - J.lo], b1 = J.nb_off[n - J.lo + 1];
-    if (!J.list && b1 - b0 > J.max_deg_here) continue;           // handled by a larger tier (uniform)
-    for (uint32_t i = tid; i < S; i += THREADS) { keys[i] = kEmpty; eta[i] = 0; inter[i] = 0; }
+    if (b1 - b0 > J.cap) {                                        // larger tier (CTA-uniform)
+      if (tid == 0) J.big_list[atomicAdd(J.big_count, 1u)] = n;
+      continue;
+    }
+    const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1], iin = i0 + J.inc_nin[n];
+    const uint32_t inn = J.in_mu[n];
+    // ---- phase 0 (P32): gcd and sum of c(e) over I(n) decide whether the packed form is exact
+    uint64_t g = 1;
+    uint32_t ib = 0;
+    if (MODE == kModeP32) {
+      uint64_t sum = 0, gg = 0;
+      for (uint64_t k = i0 + tid; k < i1; k += THREADS) {
+        const uint32_t e = J.inc[k];
+        const uint64_t a = J.edge_off[e], b = J.edge_off[e + 1];
+        const uint64_t ce = edge_c(J, e, a, b);
+        sum += ce;
+        gg = gcd64(gg, ce);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+        gg = gcd64(gg, __shfl_xor_sync(0xFFFFFFFFu, gg, o));
+      }
+      if (lane == 0) { s_sum[w] = sum; s_g[w] = gg; }
+      __syncthreads();
+      if (tid == 0) {
+        uint64_t S1 = 0, G1 = 0;
+        for (uint32_t q = 0; q < NW; ++q) { S1 += s_sum[q]; G1 = gcd64(G1, s_g[q]); }
+        if (G1 == 0) G1 = 1;
+        const uint32_t bits = inn ? 32 - __clz(inn) : 0;
+        const unsigned __int128 need = ((unsigned __int128)(S1 / G1 + 1)) << bits;
+        s_defer = need > ((unsigned __int128)1 << 32);
+        s_gcd = G1;
+        s_ib = bits;
+        if (s_defer) J.wide_list[atomicAdd(J.wide_count, 1u)] = n;
+      }
+      __syncthreads();
+      if (s_defer) continue;                                      // CTA-uniform
+      g = s_gcd;
+      ib = s_ib;
+    }
+    // ---- phase 1: bins = unflagged neighbours (+ n itself in P32 mode: every self-visit then
+    // hits a real slot, no per-pin test; misses of purged neighbours go to a trash slot S)
+    for (uint32_t i = tid; i < S; i += THREADS) {
+      keys[i] = kEmpty;
+      acc[i] = 0;
+      if (MODE == kModeWide) eta[i] = 0;
+    }
+    if (MODE == kModeP32 && tid == 0) acc[S] = 0;
     __syncthreads();
-    for (uint64_t k = b0 + tid; k < b1; k += THREADS) {          // bins = unflagged neighbours
+    for (uint64_t k = b0 + tid; k < b1; k += THREADS) {
       const uint32_t v = J.nbr[k];
       if (!(v & kPurge)) hs_insert(keys, log2s, v);
     }
+    if (MODE == kModeP32 && tid == 0) hs_insert(keys, log2s, n);
     __syncthreads();
-    // traverse I(n): warp per incident edge, lanes over its pins (Eq.4 nesting)
-    const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1], iin = i0 + J.inc_nin[n];
-    for (uint64_t k = i0 + w; k < i1; k += NW) {
-      const uint32_t e = J.inc[k];
-      const uint64_t a = J.edge_off[e], b = J.edge_off[e + 1], s = a + J.edge_nsrc[e];
-      const uint64_t we = (uint64_t)J.edge_w[e] << HGP_FP_SHIFT;
-      const uint64_t ce = J.norm ? we : we / (b - a);
-      const uint32_t mu_in = k < iin ? J.edge_mu[e] : 0u;       // e in in(n)
-      for (uint64_t j = a + lane; j < b; j += 32) {
-        const uint32_t m = J.pins[j];
-        if (m == n) continue;
-        const uint32_t slot = hs_find(keys, log2s, m);
-        if (slot == kNone) continue;                              // purged neighbour
-        atomicAdd(reinterpret_cast<unsigned long long *>(&eta[slot]), (unsigned long long)ce);
-        if (mu_in && j >= s) atomicAdd(&inter[slot], mu_in);
+    // ---- phase 2: traverse I(n): a warp loads the metadata of 32 incident edges at
+    // once (lane = edge), then walks them; pins are fetched 128 at a time (4 per lane in flight).
+    // Incident edges are dealt round-robin to warps (edge i0 + w + NW*l, l = 0, 1, ...): balanced.
+    const uint32_t keys_s = smem_u32addr(keys), acc_s = smem_u32addr(acc);
+    const uint32_t hmask = S - 1, hshift = 32u - log2s;
+    for (uint64_t kb = i0 + w; kb < i1; kb += (uint64_t)NW * 32) {
+      const uint64_t k = kb + (uint64_t)NW * lane;
+      uint64_t a = 0, ce = 0;
+      uint32_t len = 0, srel = 0, mu_in = 0;
+      if (k < i1) {
+        const uint32_t e = J.inc[k];
+        a = J.edge_off[e];
+        const uint64_t b = J.edge_off[e + 1];
+        len = (uint32_t)(b - a);
+        srel = J.edge_nsrc[e];
+        ce = edge_c(J, e, a, b);
+        mu_in = k < iin ? J.edge_mu[e] : 0u;                       // e in in(n)
+      }
+      uint32_t add_s = 0, add_d = 0;
+      if (MODE == kModeP32) {
+        add_s = (uint32_t)((ce / g) << ib);
+        add_d = add_s + mu_in;                                     // m in dst(e) and e in in(n)
+      }
+      const uint32_t cnt = (uint32_t)min((uint64_t)32, (i1 - kb + NW - 1) / NW);
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const uint64_t aj = __shfl_sync(0xFFFFFFFFu, a, j);
+        const uint32_t lj = __shfl_sync(0xFFFFFFFFu, len, j);
+        const uint32_t sj = __shfl_sync(0xFFFFFFFFu, srel, j);
+        uint32_t as_j = 0, ad_j = 0, mu_j = 0;
+        uint64_t ce_j = 0;
+        if (MODE == kModeP32) {
+          as_j = __shfl_sync(0xFFFFFFFFu, add_s, j);
+          ad_j = __shfl_sync(0xFFFFFFFFu, add_d, j);
+        } else {
+          ce_j = __shfl_sync(0xFFFFFFFFu, ce, j);
+          mu_j = __shfl_sync(0xFFFFFFFFu, mu_in, j);
+        }
+        const uint32_t *pj = J.pins + aj;
+        for (uint32_t b4 = 0; b4 < lj; b4 += 128) {
+          uint32_t m[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t idx = b4 + u * 32 + lane;
+            m[u] = idx < lj ? __ldg(pj + idx) : kEmpty;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (m[u] == kEmpty) continue;
+            const bool dst = b4 + u * 32 + lane >= sj;
+            if (MODE == kModeP32) {
+              uint32_t slot = (m[u] * 0x9E3779B1u) >> hshift;
+              while (true) {
+                const uint32_t kk = lds_u32(keys_s + 4 * slot);
+                if (kk == m[u]) break;
+                if (kk == kEmpty) { slot = S; break; }                 // purged neighbour -> trash
+                slot = (slot + 1) & hmask;
+              }
+              red_add_u32(acc_s + 4 * slot, dst ? ad_j : as_j);
+            } else {
+              if (m[u] == n) continue;
+              const uint32_t slot = hs_find(keys, log2s, m[u]);
+              if (slot == kNone) continue;                          // purged neighbour
+              atomicAdd(reinterpret_cast<unsigned long long *>(&eta[slot]), (unsigned long long)ce_j);
+              if (dst && mu_j) atomicAdd(&acc[slot], mu_j);
+            }
+          }
+        }
       }
     }
     __syncthreads();
-    // validity, purge flags, noise, per-thread top-pi
-    Top top;
+    // ---- phase 3: validity (Eq.6), purge flags, noise, per-thread top-pi
+    Top<PIMAX> top;
 #pragma unroll
-    for (int i = 0; i < HGP_MAX_PI; ++i) { top.s[i] = 0; top.id[i] = kNone; }
-    const uint64_t wn = J.node_w[n], inn = J.in_mu[n];
+    for (int i = 0; i < PIMAX; ++i) { top.s[i] = 0; top.id[i] = kNone; }
+    const uint64_t wn = J.node_w[n];
+    const uint32_t imask = ib ? (uint32_t)((1ull << ib) - 1) : 0u;
     for (uint64_t k = b0 + tid; k < b1; k += THREADS) {
       const uint32_t v = J.nbr[k];
       if (v & kPurge) continue;
       const uint32_t slot = hs_find(keys, log2s, v);
-      const uint64_t uni = inn + J.in_mu[v] - inter[slot];        // |in(n) ∪ in(m)|
+      uint64_t e_nm, inter;
+      if (MODE == kModeP32) {
+        const uint32_t x = acc[slot];
+        e_nm = (uint64_t)(ib < 32 ? x >> ib : 0) * g;
+        inter = x & imask;
+      } else {
+        e_nm = eta[slot];
+        inter = acc[slot];
+      }
+      const uint64_t uni = (uint64_t)inn + J.in_mu[v] - inter;    // |in(n) ∪ in(m)|
       const bool ok = wn + J.node_w[v] <= J.omega && (J.delta == HGP_UNBOUNDED || uni <= J.delta);
       if (!ok) { J.nbr[k] = v | kPurge; continue; }
-      uint64_t sc = eta[slot];
+      uint64_t sc = e_nm;
       if (J.noise_cap) {
         const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
-        sc += splitmix64(key ^ J.seed_mix) % (J.noise_cap + 1);
+        sc += __umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);   // uniform in [0, cap]
       }
-      top_insert(top, J.pi, sc, v);
+      top_insert<PIMAX>(top, J.pi, sc, v);
     }
-    // CTA-wide merge of the per-thread lists: pi rounds of argmax over list heads
-    uint32_t head = 0;
-    for (uint32_t r = 0; r < J.pi; ++r) {
-      uint64_t hs = 0;
-      uint32_t hid = kNone;
+    // ---- phase 4: warp-level merges (pi rounds of shuffle argmax over list heads), then warp 0
+    // merges the NW warp lists the same way; two barriers per node
+    warp_top_merge<PIMAX>(top, J.pi, s_tops + w * PIMAX, s_topi + w * PIMAX);
+    __syncthreads();
+    if (w == 0) {
+      Top<PIMAX> t2;
 #pragma unroll
-      for (int i = 0; i < HGP_MAX_PI; ++i)
-        if (i == (int)head) { hs = top.s[i]; hid = top.id[i]; }
-      uint32_t who = tid;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t os = __shfl_xor_sync(0xFFFFFFFFu, hs, o);
-        const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, hid, o);
-        const uint32_t ow = __shfl_xor_sync(0xFFFFFFFFu, who, o);
-        if (better(os, oi, hs, hid)) { hs = os; hid = oi; who = ow; }
+      for (int i = 0; i < PIMAX; ++i) { t2.s[i] = 0; t2.id[i] = kNone; }
+      for (uint32_t i = lane; i < NW * J.pi; i += 32) {
+        const uint32_t ww = i / J.pi, r = i % J.pi;
+        top_insert<PIMAX>(t2, J.pi, s_tops[ww * PIMAX + r], s_topi[ww * PIMAX + r]);
       }
-      if (lane == 0) { red_s[w] = hs; red_i[w] = hid; red_t[w] = who; }
-      __syncthreads();
-      if (tid == 0) {
-        uint64_t bs = red_s[0];
-        uint32_t bi = red_i[0], bt = red_t[0];
-        for (uint32_t q = 1; q < NW; ++q)
-          if (better(red_s[q], red_i[q], bs, bi)) { bs = red_s[q]; bi = red_i[q]; bt = red_t[q]; }
+      warp_top_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX, s_topi + NW * PIMAX);
+      __syncwarp();
+      for (uint32_t r = lane; r < J.pi; r += 32) {
         hgp_cand cd;
-        cd.id = bi; cd.pad = 0; cd.score = bi == kNone ? 0 : bs;
+        cd.id = s_topi[NW * PIMAX + r];
+        cd.pad = 0;
+        cd.score = cd.id == kNone ? 0 : s_tops[NW * PIMAX + r];
         J.cand[(uint64_t)n * J.pi + r] = cd;
-        s_win = bi == kNone ? kNone : bt;
       }
-      __syncthreads();
-      if (s_win == tid) ++head;
     }
     __syncthreads();
-  }
-}
-
-__global__ void k_score_classify(const uint64_t *nb_off, uint32_t lo, uint32_t hi, uint32_t capA, uint32_t capB,
-                                 uint32_t *listB, uint32_t *listC, uint32_t *counts) {
-  for (uint32_t n = lo + blockIdx.x * blockDim.x + threadIdx.x; n < hi; n += gridDim.x * blockDim.x) {
-    const uint64_t d = nb_off[n - lo + 1] - nb_off[n - lo];
-    if (d > capA) {
-      if (d <= capB) listB[atomicAdd(&counts[0], 1u)] = n;
-      else listC[atomicAdd(&counts[1], 1u)] = n;
-    }
   }
 }
 
@@ -184,8 +331,55 @@ __global__ void k_score_check(const uint32_t *node_w, const uint32_t *in_mu, uin
   }
 }
 
-static constexpr uint32_t kSALog = 11, kSAThreads = 128;   // 2048 slots x 16 B = 32 KB, <= 1024 entries
-static constexpr uint32_t kSBLog = 13, kSBThreads = 256;   // 8192 slots = 128 KB, <= 4096 entries
+// tiers: A = 4096-slot shared table (<= 2048 entries, 32 KB), B = 16384 slots (<= 8192, 128 KB),
+// W = wide accumulators (4096 slots x 16 B = 64 KB), H = global-memory tables (any size, wide)
+static constexpr uint32_t kSALog = 12, kSAThreads = 128;
+static constexpr uint32_t kSBLog = 14, kSBThreads = 256;
+static constexpr uint32_t kSWLog = 12, kSWThreads = 256;
+
+template <int PIMAX>
+hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_deg, uint32_t *lists,
+                              uint32_t *counts) {
+  hgp_status st = HGP_OK;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_score<kSAThreads, kModeP32, true, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (8 << kSALog) + 16);
+    cudaFuncSetAttribute(k_score<kSBThreads, kModeP32, true, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (8 << kSBLog) + 16);
+    cudaFuncSetAttribute(k_score<kSWThreads, kModeWide, true, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         16 << kSWLog);
+    attr = true;
+  }
+  uint32_t *bigA = lists, *wide = lists + nn, *huge = lists + 2 * (size_t)nn;
+  // A: every node; larger neighbourhoods -> bigA, packed overflow -> wide
+  J.list = nullptr; J.list_count = nullptr; J.cap = 1u << (kSALog - 1); J.log2s = kSALog;
+  J.big_list = bigA; J.big_count = counts + 0; J.wide_list = wide; J.wide_count = counts + 1;
+  const uint32_t gA = nn < 64u * c->sm_count ? nn : 64u * c->sm_count;
+  HGP_TRY(launch(c, "score_A", k_score<kSAThreads, kModeP32, true, PIMAX>, dim3(gA), dim3(kSAThreads), (8u << kSALog) + 16,
+                 J));
+  if (max_deg > (1u << (kSALog - 1))) {   // B: big neighbourhoods, packed
+    J.list = bigA; J.list_count = counts + 0; J.cap = 1u << (kSBLog - 1); J.log2s = kSBLog;
+    J.big_list = huge; J.big_count = counts + 2;
+    HGP_TRY(launch(c, "score_B", k_score<kSBThreads, kModeP32, true, PIMAX>, dim3(c->sm_count), dim3(kSBThreads),
+                   (8u << kSBLog) + 16, J));
+  }
+  // W: nodes whose packed sums could overflow 32 bits (neighbourhoods up to 2048)
+  J.list = wide; J.list_count = counts + 1; J.cap = 1u << (kSWLog - 1); J.log2s = kSWLog;
+  J.big_list = huge; J.big_count = counts + 2;
+  HGP_TRY(launch(c, "score_W", k_score<kSWThreads, kModeWide, true, PIMAX>, dim3(c->sm_count), dim3(kSWThreads),
+                 16u << kSWLog, J));
+  if (max_deg > (1u << (kSWLog - 1))) {   // H: global-memory wide tables
+    uint32_t lg = kSWLog;
+    while ((1u << (lg - 1)) < max_deg) ++lg;
+    const uint32_t ctas = c->sm_count;
+    uint32_t *gtab = scratch_raw<uint32_t>(c, ((size_t)ctas * 16 << lg) / 4, &st);
+    if (st) return st;
+    J.list = huge; J.list_count = counts + 2; J.cap = 0xFFFFFFFFu; J.log2s = lg; J.gtab = gtab;
+    HGP_TRY(launch(c, "score_H", k_score<256, kModeWide, false, PIMAX>, dim3(ctas), dim3(256), 0, J));
+  }
+  return HGP_OK;
+}
 
 }  // namespace hgp
 
@@ -229,33 +423,11 @@ extern "C" hgp_status hgp_score_pairs(hgp_ctx *c, const hgp_csr *g, hgp_nbrs *nb
   J.omega = p->omega; J.delta = p->delta; J.noise_cap = p->noise_cap;
   J.seed_mix = splitmix64_host(p->noise_seed);
   J.pi = p->pi; J.norm = p->norm; J.cand = cand;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_score<kSAThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 << kSALog);
-    cudaFuncSetAttribute(k_score<kSBThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 << kSBLog);
-    attr = true;
-  }
-  const uint32_t capA = 1u << (kSALog - 1), capB = 1u << (kSBLog - 1);
-  // tier A: every node whose neighbourhood fits 1024 entries
-  J.list = nullptr; J.list_count = nullptr; J.max_deg_here = capA; J.log2s = kSALog;
-  const uint32_t gA = nn < 64u * c->sm_count ? nn : 64u * c->sm_count;
-  HGP_TRY(launch(c, "score_A", k_score<kSAThreads, true>, dim3(gA), dim3(kSAThreads), 16u << kSALog, J));
-  if (nb->max_deg > capA) {
-    uint32_t *lists = scratch_raw<uint32_t>(c, 2 * (size_t)nn, &st);
-    if (st) return st;
-    HGP_TRY(launch(c, "score_classify", k_score_classify, dim3(div_up(nn, 256) < 1024 ? div_up(nn, 256) : 1024),
-                   dim3(256), 0, (const uint64_t *)nb->off, lo, hi, capA, capB, lists, lists + nn, counts));
-    J.list = lists; J.list_count = counts; J.max_deg_here = capB; J.log2s = kSBLog;
-    HGP_TRY(launch(c, "score_B", k_score<kSBThreads, true>, dim3(c->sm_count), dim3(kSBThreads), 16u << kSBLog, J));
-    if (nb->max_deg > capB) {
-      uint32_t lg = kSBLog;
-      while ((1u << (lg - 1)) < nb->max_deg) ++lg;
-      const uint32_t ctas = c->sm_count;
-      uint32_t *gtab = scratch_raw<uint32_t>(c, ((size_t)ctas * 16 << lg) / 4, &st);
-      if (st) return st;
-      J.list = lists + nn; J.list_count = counts + 1; J.max_deg_here = 1u << (lg - 1); J.log2s = lg; J.gtab = gtab;
-      HGP_TRY(launch(c, "score_C", k_score<256, false>, dim3(ctas), dim3(256), 0, J));
-    }
+  uint32_t *lists = scratch_raw<uint32_t>(c, 3 * (size_t)(nn ? nn : 1), &st);
+  if (st) return st;
+  if (nn) {
+    if (p->pi <= 4) HGP_TRY(launch_score_tiers<4>(c, J, nn, nb->max_deg, lists, counts));
+    else HGP_TRY(launch_score_tiers<16>(c, J, nn, nb->max_deg, lists, counts));
   }
   uint64_t err[kErrSlots];
   HGP_TRY(fetch_errors(c, err));

@@ -71,7 +71,7 @@ def noise(n, m, seed, cap):
     if cap == 0:
         return 0
     key = (min(n, m) << 32) | max(n, m)
-    return splitmix64(key ^ splitmix64(seed)) % (cap + 1)
+    return (splitmix64(key ^ splitmix64(seed)) * (cap + 1)) >> 64
 
 
 def score_bruteforce(N, edge_off, edge_nsrc, pins, edge_w, edge_mu, node_w, omega, delta, pi,
