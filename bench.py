@@ -59,12 +59,14 @@ def algorithmic_bytes(step: str, N, E, P, V, pi, Nc=0, Ec=0, Pc=0, Vc=0) -> int:
         return 4 * V + 8 * P + 20 * E + 28 * N + 16 * pi * N
     if step == "a4":
         return 16 * pi * N + 4 * N
+    if step == "a2+a3":   # fused: a3's reads + the write of N(n) instead of its read
+        return 8 * P + 20 * E + 28 * N + 4 * V + 16 * pi * N
     if step == "a5":
         return 16 * N + 4 * P + 20 * E + 8 * Pc + 20 * Ec + 4 * V + 4 * Vc + 28 * Nc
     raise KeyError(step)
 
 
-KERNEL_STEP = {"validate": "a1", "check": "a1", "segsort": "a1", "inc_": "a1", "fill_mu": "a1", "max_deg": "a1",
+KERNEL_STEP = {"nbrscore": "a2+a3", "pairs_total": "a2+a3", "fused_pack": "a2+a3", "validate": "a1", "check": "a1", "segsort": "a1", "inc_": "a1", "fill_mu": "a1", "max_deg": "a1",
                "edge_pairs": "a2", "nbrs_": "a2", "nbr_": "a2", "score_": "a3", "round_": "a4", "jump_": "a4",
                "fill_none": "a4"}
 
@@ -232,8 +234,7 @@ def main():
 
     def step(inp):
         g = hgp.build_csr(ctx, N, inp["edge_off"], inp["edge_nsrc"], inp["pins"], inp["edge_w"], inp["node_w"])
-        nb = hgp.unique_neighbors(ctx, g)
-        cg, cnb, st = hgp.coarsen_level(ctx, g, nb, params, cand, match, gamma)
+        nb, cg, cnb, st = hgp.coarsen_level0(ctx, g, params, cand, match, gamma)
         last.update(st=st, V=nb.V, max_deg=nb.c.max_deg)
         for x in (g, nb, cg, cnb):
             x.free()
@@ -341,7 +342,7 @@ def main():
         "step_ms": {k: round(v, 4) for k, v in sorted(step_ms.items())},
         "kernels_ms": {k: round(v[0], 4) for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0])[:12]},
         "level_hbm_frac": sum(algorithmic_bytes(s, N, E, P, V, pi, st["Nc"], st["Ec"], st["Pc"], st["Vc"])
-                              for s in ("a1", "a2", "a3", "a4", "a5")) / (ms * 1e-3) / 1e9 / peak,
+                              for s in ("a1", "a2+a3", "a4", "a5")) / (ms * 1e-3) / 1e9 / peak,
     }
     if e2e:
         line["e2e"] = e2e

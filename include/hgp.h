@@ -191,6 +191,20 @@ HGP_API hgp_status hgp_coarsen_level(hgp_ctx *ctx, const hgp_csr *g, hgp_nbrs *n
                                      hgp_cand *cand, uint32_t *match, uint32_t *gamma, hgp_csr *coarse,
                                      hgp_nbrs *coarse_nb, hgp_level_stats *stats);
 
+/* a2 + a3 fused for a level whose neighbour lists carry no flags yet (the first level): one
+ * traversal of I(n) builds N(n) and its histogram together (see level0.cu). Outputs are
+ * identical to hgp_unique_neighbors(g, 0, N) followed by hgp_score_pairs; nodes the fused
+ * kernel cannot represent make the call run that unfused pair instead. nb is allocated by
+ * the library (all nodes); cand is caller [N][pi]. Synchronises. */
+HGP_API hgp_status hgp_neighbors_and_scores(hgp_ctx *ctx, const hgp_csr *g, const hgp_params *p, hgp_nbrs *nb,
+                                           hgp_cand *cand);
+
+/* The first level straight from a level-0 CSR: fused a2+a3 -> a4 -> a5. nb receives N(n) with
+ * the purge flags set by a3 (library-owned). cand may be NULL; stats (HOST) may be NULL. */
+HGP_API hgp_status hgp_coarsen_level0(hgp_ctx *ctx, const hgp_csr *g, const hgp_params *p, hgp_cand *cand,
+                                      uint32_t *match, uint32_t *gamma, hgp_nbrs *nb, hgp_csr *coarse,
+                                      hgp_nbrs *coarse_nb, hgp_level_stats *stats);
+
 HGP_API void hgp_csr_free(hgp_ctx *ctx, hgp_csr *g);
 HGP_API void hgp_nbrs_free(hgp_ctx *ctx, hgp_nbrs *nb);
 

@@ -162,6 +162,11 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
 __device__ __forceinline__ uint32_t smem_u32addr(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// keep a value in a register (stops the compiler from rematerialising, e.g., the shared window base)
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(x));
+  return x;
+}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));

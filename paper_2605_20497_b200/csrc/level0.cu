@@ -1,0 +1,409 @@
+// level0.cu — fused a2 + a3 for the first level, and hgp_coarsen_level0.
+//
+// At level 0 no neighbour carries a purge flag yet, so materialising N(n) (a2) and
+// building the histogram over it (a3) need the same single traversal of I(n) and its
+// pins: one CTA per node inserts every pin it meets into a shared-memory hash table (the set
+// N(n) ∪ {n}) and, in the same step, adds the pin's packed (c(e)/g << ib | mu-if-inbound) term to
+// the slot (native 32-bit shared atomics). Validity, flags, noise and top-Pi then run over the
+// node's unique keys, which are also appended (flags included) to N(n). This replaces two
+// traversals of the T = sum_e |e|(|e|-1) pin visits by one; results are identical to
+// hgp_unique_neighbors followed by hgp_score_pairs (same integer sums, same tie rules).
+// Nodes the packed form cannot represent, or whose neighbourhood overflows the largest shared
+// table, are handled by the unfused kernels (the whole call falls back if any node does).
+#include <cstdlib>
+
+#include "csr_impl.cuh"
+#include "hashset.cuh"
+#include "scan.cuh"
+#include "score_common.cuh"
+
+namespace hgp {
+
+struct FusedJob {
+  ScoreJob S;                     // level arrays + parameters + cand
+  const uint32_t *list, *list_count;   // nodes to process (nullptr: all of [lo, hi))
+  uint32_t log2s, cap;            // table size, max unique neighbours before overflow
+  uint32_t *pool;
+  uint64_t pool_cap;
+  unsigned long long *pool_cursor;
+  uint64_t *start;                // [hi-lo] pool offset of each node's N(n)
+  uint32_t *cnt;                  // [hi-lo]
+  uint32_t *defer_list, *defer_count;
+};
+
+template <int THREADS, int PIMAX>
+__global__ void __launch_bounds__(THREADS) k_nbrscore(FusedJob F) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ uint64_t s_tops[(THREADS / 32 + 1) * PIMAX];
+  __shared__ uint32_t s_topi[(THREADS / 32 + 1) * PIMAX];
+  __shared__ uint64_t s_sum[THREADS / 32], s_g[THREADS / 32];
+  __shared__ uint32_t s_defer, s_cnt, s_ib, s_count;
+  __shared__ uint64_t s_gcd;
+  __shared__ unsigned long long s_start;
+  constexpr uint32_t NW = THREADS / 32;
+  const ScoreJob &J = F.S;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t log2s = F.log2s, S = 1u << log2s;
+  uint32_t *keys = reinterpret_cast<uint32_t *>(dyn);
+  uint32_t *acc = keys + S;
+  uint32_t *ulist = acc + S;                                      // dense list of neighbour slots
+  const uint32_t keys_s = opaque_u32(smem_u32addr(keys)), acc_s = opaque_u32(smem_u32addr(acc));
+  const uint32_t hmask = S - 1, hshift = 32u - log2s;
+  volatile uint32_t *vcnt = &s_cnt;
+  const uint32_t total = F.list_count ? *F.list_count : J.hi - J.lo;
+  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const uint32_t n = F.list ? F.list[t] : J.lo + t;
+    const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1], iin = i0 + J.inc_nin[n];
+    const uint32_t inn = J.in_mu[n];
+    // ---- phase 0: gcd / sum of c(e) over I(n): is the packed 32-bit accumulator exact?
+    uint64_t sum = 0, gg = 0;
+    for (uint64_t k = i0 + tid; k < i1; k += THREADS) {
+      const uint32_t e = J.inc[k];
+      const uint64_t a = J.edge_off[e], b = J.edge_off[e + 1];
+      const uint64_t ce = edge_c(J, e, a, b);
+      sum += ce;
+      gg = gcd64(gg, ce);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+      gg = gcd64(gg, __shfl_xor_sync(0xFFFFFFFFu, gg, o));
+    }
+    if (lane == 0) { s_sum[w] = sum; s_g[w] = gg; }
+    for (uint32_t i = tid; i < S / 4; i += THREADS) {
+      reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+      reinterpret_cast<uint4 *>(acc)[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t S1 = 0, G1 = 0;
+      for (uint32_t q = 0; q < NW; ++q) { S1 += s_sum[q]; G1 = gcd64(G1, s_g[q]); }
+      if (G1 == 0) G1 = 1;
+      const uint32_t bits = inn ? 32 - __clz(inn) : 0;
+      const unsigned __int128 need = ((unsigned __int128)(S1 / G1 + 1)) << bits;
+      s_defer = need > ((unsigned __int128)1 << 32);
+      s_gcd = G1;
+      s_ib = bits;
+      s_cnt = 0;
+      hs_insert(keys, log2s, n);                                 // self-visits land in n's slot
+    }
+    __syncthreads();
+    if (s_defer) {
+      if (tid == 0) F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
+      __syncthreads();
+      continue;
+    }
+    const uint64_t g = s_gcd;
+    const uint32_t ib = s_ib;
+    // ---- phase 1 (= a2 + a3 traversal): insert-or-find every pin, add its packed term.
+    // New keys are counted per lane and flushed once per 128-pin block (warp reduce + one
+    // shared atomic) so that the overflow vote sees a count lagging by < 128 per warp.
+    bool stop = false;
+    uint32_t nins = 0;
+    for (uint64_t kb = i0 + w; kb < i1 && !stop; kb += (uint64_t)NW * 32) {
+      const uint64_t k = kb + (uint64_t)NW * lane;
+      uint64_t a = 0;
+      uint32_t len = 0, srel = 0, add_s = 0, add_d = 0;
+      if (k < i1) {
+        const uint32_t e = J.inc[k];
+        a = J.edge_off[e];
+        const uint64_t b = J.edge_off[e + 1];
+        len = (uint32_t)(b - a);
+        srel = J.edge_nsrc[e];
+        add_s = (uint32_t)((edge_c(J, e, a, b) / g) << ib);
+        add_d = add_s + (k < iin ? J.edge_mu[e] : 0u);             // m in dst(e), e in in(n)
+      }
+      const uint32_t cnt = (uint32_t)min((uint64_t)32, (i1 - kb + NW - 1) / NW);
+      for (uint32_t j = 0; j < cnt && !stop; ++j) {
+        const uint64_t aj = __shfl_sync(0xFFFFFFFFu, a, j);
+        const uint32_t lj = __shfl_sync(0xFFFFFFFFu, len, j);
+        const uint32_t sj = __shfl_sync(0xFFFFFFFFu, srel, j);
+        const uint32_t as_j = __shfl_sync(0xFFFFFFFFu, add_s, j);
+        const uint32_t ad_j = __shfl_sync(0xFFFFFFFFu, add_d, j);
+        const uint32_t *pj = J.pins + aj;
+        for (uint32_t b4 = 0; b4 < lj; b4 += 128) {
+          if (__any_sync(0xFFFFFFFFu, *vcnt >= F.cap)) { stop = true; break; }   // warp-uniform vote
+          uint32_t m[4], sl[4], kk[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t idx = b4 + u * 32 + lane;
+            m[u] = idx < lj ? __ldg(pj + idx) : kEmpty;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) sl[u] = (m[u] * 0x9E3779B1u) >> hshift;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) kk[u] = lds_u32(keys_s + 4 * sl[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (m[u] == kEmpty) continue;
+            uint32_t slot = sl[u], k2 = kk[u];
+            while (k2 != m[u]) {
+              if (k2 == kEmpty) {
+                k2 = cas_u32(keys_s + 4 * slot, kEmpty, m[u]);
+                if (k2 == kEmpty) { ++nins; break; }
+                continue;                                           // re-test the winner's key
+              }
+              slot = (slot + 1) & hmask;
+              k2 = lds_u32(keys_s + 4 * slot);
+            }
+            red_add_u32(acc_s + 4 * slot, b4 + u * 32 + lane >= sj ? ad_j : as_j);
+          }
+          const uint32_t tins = __reduce_add_sync(0xFFFFFFFFu, nins);
+          if (lane == 0 && tins) atomicAdd(&s_cnt, tins);
+          nins = 0;
+        }
+      }
+    }
+    if (stop && lane == 0) s_defer = 1;
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t c0 = s_cnt;
+      s_count = c0;
+      if (!s_defer) {
+        const unsigned long long st = atomicAdd(F.pool_cursor, (unsigned long long)c0);
+        s_start = st;
+        if (st + c0 > F.pool_cap) s_defer = 1;
+      }
+      s_cnt = 0;                                                  // reused as the compaction cursor
+    }
+    __syncthreads();
+    const uint32_t count = s_count;
+    if (s_defer) {
+      if (tid == 0) F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
+      __syncthreads();
+      continue;
+    }
+    // ---- phase 2a: compact the occupied slots (but n's) into a dense list: warps sweep 32
+    // consecutive slots at a time (conflict-free) with a ballot and one shared atomic per chunk
+    const uint32_t lt = (1u << lane) - 1;
+    for (uint32_t sb = w * 32; sb < S; sb += NW * 32) {
+      const uint32_t v = keys[sb + lane];
+      const bool has = v != kEmpty && v != n;
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, has);
+      if (!bal) continue;
+      uint32_t wpos = 0;
+      if (lane == 0) wpos = atomicAdd(&s_cnt, __popc(bal));
+      wpos = __shfl_sync(0xFFFFFFFFu, wpos, 0);
+      if (has) ulist[wpos + __popc(bal & lt)] = sb + lane;
+    }
+    __syncthreads();
+    // ---- phase 2b: validity (Eq.6), flags, the N(n) entries with their flags,
+    // noise, per-thread top-pi
+    Top<PIMAX> top;
+#pragma unroll
+    for (int i = 0; i < PIMAX; ++i) { top.s[i] = 0; top.id[i] = 0; }
+    const uint64_t wn = J.node_w[n];
+    const uint32_t imask = ib ? (uint32_t)((1ull << ib) - 1) : 0u;
+    const uint64_t base = s_start;
+    for (uint32_t i = tid; i < count; i += THREADS) {
+      const uint32_t slot = ulist[i];
+      const uint32_t v = keys[slot];
+      const uint32_t x = acc[slot];
+      const uint64_t e_nm = (uint64_t)(ib < 32 ? x >> ib : 0) * g;
+      const uint64_t inter = x & imask;
+      const uint64_t uni = (uint64_t)inn + J.in_mu[v] - inter;    // |in(n) ∪ in(m)|
+      const bool ok = wn + J.node_w[v] <= J.omega && (J.delta == HGP_UNBOUNDED || uni <= J.delta);
+      F.pool[base + i] = ok ? v : (v | kPurge);
+      if (!ok) continue;
+      uint64_t sc = e_nm;
+      if (J.noise_cap) {
+        const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
+        sc += __umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);   // uniform in [0, cap]
+      }
+      top_insert<PIMAX>(top, J.pi, sc, v);
+    }
+    if (tid == 0) { F.start[n - J.lo] = base; F.cnt[n - J.lo] = count; }
+    // ---- phase 3: top-pi merge (warps, then warp 0)
+    warp_top_merge<PIMAX>(top, J.pi, s_tops + w * PIMAX, s_topi + w * PIMAX);
+    __syncthreads();
+    if (w == 0) {
+      Top<PIMAX> t2;
+#pragma unroll
+      for (int i = 0; i < PIMAX; ++i) { t2.s[i] = 0; t2.id[i] = 0; }
+      for (uint32_t i = lane; i < NW * J.pi; i += 32) {
+        const uint32_t ww = i / J.pi, r = i % J.pi;
+        top_insert<PIMAX>(t2, J.pi, s_tops[ww * PIMAX + r], s_topi[ww * PIMAX + r]);
+      }
+      warp_top_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX, s_topi + NW * PIMAX);
+      __syncwarp();
+      for (uint32_t r = lane; r < J.pi; r += 32) {
+        hgp_cand cd;
+        cd.score = s_tops[NW * PIMAX + r];
+        cd.id = cd.score ? s_topi[NW * PIMAX + r] : kNone;
+        cd.pad = 0;
+        J.cand[(uint64_t)n * J.pi + r] = cd;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_fused_pack(const uint32_t *pool, const uint64_t *start, const uint32_t *cnt, const uint64_t *off,
+                             uint32_t nn, uint32_t *nbr, unsigned int *maxdeg) {
+  const uint32_t lane = lane_id();
+  uint32_t mx = 0;
+  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < nn; t += gridDim.x * (blockDim.x >> 5)) {
+    const uint32_t c = cnt[t];
+    const uint32_t *src = pool + start[t];
+    uint32_t *dst = nbr + off[t];
+    for (uint32_t j = lane; j < c; j += 32) dst[j] = src[j];
+    mx = max(mx, c);
+  }
+  mx = warp_max(mx);
+  if (lane == 0) atomicMax(maxdeg, mx);
+}
+
+__global__ void k_pairs_total(const uint64_t *edge_off, uint32_t E, unsigned long long *T) {
+  uint64_t s = 0;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const uint64_t d = edge_off[e + 1] - edge_off[e];
+    s += d * (d - 1);
+  }
+  s = warp_sum(s);
+  if (lane_id() == 0) atomicAdd(T, (unsigned long long)s);
+}
+
+// tiers of the fused kernel: 4096 slots (40 KB incl. list, 128 threads) for every node, then
+// 16384 slots (160 KB, 256 threads) for the ones that overflowed
+static constexpr uint32_t kFALog = 12, kFAThreads = 128;
+static constexpr uint32_t kFBLog = 14, kFBThreads = 256;
+
+template <int PIMAX, int TA>
+hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, uint32_t nn, uint32_t *lists, uint32_t *counts) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_nbrscore<TA, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 10 << kFALog);
+    cudaFuncSetAttribute(k_nbrscore<kFBThreads, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 10 << kFBLog);
+    attr = true;
+  }
+  F.list = nullptr; F.list_count = nullptr; F.log2s = kFALog;
+  F.cap = (1u << (kFALog - 1)) - 128 * (TA / 32) - 1;
+  F.defer_list = lists; F.defer_count = counts + 0;
+  const uint32_t per_sm = TA == 128 ? 32u : 16u;
+  const uint32_t gA = nn < per_sm * c->sm_count ? nn : per_sm * c->sm_count;
+  HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX>, dim3(gA), dim3(TA), 10u << kFALog, F));
+  F.list = lists; F.list_count = counts + 0; F.log2s = kFBLog;
+  F.cap = (1u << (kFBLog - 1)) - 128 * (kFBThreads / 32) - 1;
+  F.defer_list = lists + nn; F.defer_count = counts + 1;
+  HGP_TRY(launch(c, "nbrscore_B", k_nbrscore<kFBThreads, PIMAX>, dim3(c->sm_count), dim3(kFBThreads),
+                 10u << kFBLog, F));
+  return HGP_OK;
+}
+
+template <int PIMAX>
+hgp_status fused_tiers(hgp_ctx *c, FusedJob F, uint32_t nn, uint32_t *lists, uint32_t *counts) {
+  static const int threads = getenv("HGP_FUSED_THREADS") ? atoi(getenv("HGP_FUSED_THREADS")) : 256;
+  if (threads == 128) return fused_tiers_t<PIMAX, 128>(c, F, nn, lists, counts);
+  return fused_tiers_t<PIMAX, 256>(c, F, nn, lists, counts);
+}
+
+// a2 + a3 on a level-0 CSR (no flags yet). Returns the same nb and cand as hgp_unique_neighbors
+// followed by hgp_score_pairs. Synchronises.
+hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, hgp_nbrs *out, hgp_cand *cand) {
+  memset(out, 0, sizeof(*out));
+  const uint32_t nn = g->N;
+  ScoreJob J;
+  HGP_TRY(score_prologue(c, g, 0, nn, p, &J));
+  J.cand = cand;
+  hgp_status st = HGP_OK;
+  unsigned long long *misc = scratch_zero<unsigned long long>(c, 2, &st);    // T, pool cursor
+  uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
+  uint64_t *start = scratch_raw<uint64_t>(c, nn, &st);
+  uint32_t *cnt = scratch_raw<uint32_t>(c, nn, &st);
+  uint32_t *lists = scratch_raw<uint32_t>(c, 2 * (size_t)(nn ? nn : 1), &st);
+  if (st) return st;
+  if (nn == 0) return HGP_E_INTERNAL;   // handled by the caller's fallback
+  HGP_TRY(launch(c, "pairs_total", k_pairs_total, dim3(g->E ? (div_up(g->E, 256) < 1024 ? div_up(g->E, 256) : 1024) : 0),
+                 dim3(256), 0, (const uint64_t *)g->edge_off, g->E, misc));
+  uint64_t T = 0;
+  HGP_TRY(read_u64(c, (const uint64_t *)misc, &T));
+  uint64_t pool_cap = T < 24 * g->P + nn ? T : 24 * g->P + nn;
+  if (pool_cap == 0) pool_cap = 1;
+  uint32_t *pool = scratch_raw<uint32_t>(c, pool_cap, &st);
+  if (st) return st;
+  FusedJob F{};
+  F.S = J;
+  F.pool = pool; F.pool_cap = pool_cap; F.pool_cursor = misc + 1; F.start = start; F.cnt = cnt;
+  if (p->pi <= 4) HGP_TRY(fused_tiers<4>(c, F, nn, lists, counts));
+  else HGP_TRY(fused_tiers<16>(c, F, nn, lists, counts));
+  uint32_t hc[2];
+  HGP_TRY(read_back(c, counts, 8, hc));
+  if (hc[1]) return HGP_E_INTERNAL;      // some node needs the unfused path: caller falls back
+  HGP_TRY(score_finish(c));
+  out->lo = 0;
+  out->hi = nn;
+  out->off = dalloc_n<uint64_t>(c, (size_t)nn + 1, &st);
+  if (st) return st;
+  uint64_t V = 0;
+  HGP_TRY(scan_exclusive(c, InU32{cnt}, nn, out->off, &V));
+  out->V = V;
+  out->nbr = dalloc_n<uint32_t>(c, V, &st);
+  if (st) return st;
+  unsigned int *d_max = counts + 2;
+  HGP_TRY(launch(c, "fused_pack", k_fused_pack, dim3(nn / 8 + 1 < 16u * c->sm_count ? nn / 8 + 1 : 16u * c->sm_count),
+                 dim3(256), 0, (const uint32_t *)pool, (const uint64_t *)start, (const uint32_t *)cnt,
+                 (const uint64_t *)out->off, nn, out->nbr, d_max));
+  uint32_t mx = 0;
+  HGP_TRY(read_back(c, d_max, 4, &mx));
+  out->max_deg = mx;
+  return HGP_OK;
+}
+
+hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match, uint32_t *gamma,
+                         hgp_csr *C, hgp_nbrs *CN, hgp_level_stats *stats);
+
+}  // namespace hgp
+
+using namespace hgp;
+
+extern "C" hgp_status hgp_neighbors_and_scores(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, hgp_nbrs *nb,
+                                               hgp_cand *cand) {
+  if (!c || !g || !p || !nb || !cand) return set_error(HGP_E_ARG, "hgp_neighbors_and_scores: null argument");
+  ApiScope scope(c);
+  hgp_status s = g->N ? nbrs_score_fused(c, g, p, nb, cand) : HGP_E_INTERNAL;
+  if (s == HGP_OK) return HGP_OK;
+  if (s != HGP_E_INTERNAL) { free_nbrs(c, nb); return s; }
+  // unfused path: a2 then a3 (identical results)
+  free_nbrs(c, nb);
+  HGP_TRY(hgp_unique_neighbors(c, g, 0, g->N, nb));
+  s = score_run(c, g, nb, p, cand, nullptr, nullptr);
+  if (s != HGP_OK) free_nbrs(c, nb);
+  return s;
+}
+
+extern "C" hgp_status hgp_coarsen_level0(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, hgp_cand *cand,
+                                         uint32_t *match, uint32_t *gamma, hgp_nbrs *nb, hgp_csr *coarse,
+                                         hgp_nbrs *coarse_nb, hgp_level_stats *stats) {
+  if (!c || !g || !p || !match || !gamma || !nb || !coarse || !coarse_nb)
+    return set_error(HGP_E_ARG, "hgp_coarsen_level0: null argument");
+  if (p->pi < 1 || p->pi > HGP_MAX_PI) return set_error(HGP_E_ARG, "pi must be in [1,16]");
+  ApiScope scope(c);
+  hgp_status st = HGP_OK;
+  if (!cand) {
+    cand = scratch_raw<hgp_cand>(c, (size_t)g->N * p->pi, &st);
+    if (st) return st;
+  }
+  uint32_t *per = scratch_zero<uint32_t>(c, HGP_MAX_PI, &st);
+  if (st) return st;
+  HGP_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  HGP_TRY(hgp_neighbors_and_scores(c, g, p, nb, cand));
+  HGP_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  hgp_status s = hgp_match(c, cand, g->N, p->pi, match, per);
+  if (s != HGP_OK) { free_nbrs(c, nb); return s; }
+  HGP_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  s = contract_impl(c, g, nb, match, gamma, coarse, coarse_nb, stats);
+  if (s != HGP_OK) { free_csr(c, coarse); free_nbrs(c, coarse_nb); free_nbrs(c, nb); return s; }
+  HGP_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  HGP_CUDA(cudaEventSynchronize(c->ev[3]));
+  if (stats) {
+    stats->N = g->N; stats->E = g->E; stats->P = g->P; stats->V = nb->V;
+    uint32_t hper[HGP_MAX_PI];
+    HGP_TRY(read_back(c, per, sizeof(hper), hper));
+    for (int i = 0; i < HGP_MAX_PI; ++i) stats->matched_per_round[i] = i < (int)p->pi ? hper[i] : 0;
+    cudaEventElapsedTime(&stats->ms[0], c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&stats->ms[1], c->ev[1], c->ev[2]);
+    cudaEventElapsedTime(&stats->ms[2], c->ev[2], c->ev[3]);
+    cudaEventElapsedTime(&stats->ms[3], c->ev[0], c->ev[3]);
+  }
+  return HGP_OK;
+}

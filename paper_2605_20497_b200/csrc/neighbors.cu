@@ -40,9 +40,7 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
   constexpr uint32_t NW = THREADS / 32;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t S = 1u << J.log2s;
-  // table of S slots followed by the append list of inserted keys (<= S/2 by the cap)
-  uint32_t *tab = SMEM ? dyn : J.gtab + (size_t)blockIdx.x * (((size_t)3 << J.log2s) >> 1);
-  uint32_t *ulist = tab + S;
+  uint32_t *tab = SMEM ? dyn : J.gtab + ((size_t)blockIdx.x << J.log2s);
   const uint32_t total = J.list_count ? *J.list_count : J.nall;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = J.list ? J.list[t] : J.lo + t;
@@ -52,7 +50,10 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
     __syncthreads();
     const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1];
     volatile uint32_t *vcnt = &s_cnt;
+    const uint32_t tab_s = SMEM ? opaque_u32(smem_u32addr(tab)) : 0u;
+    const uint32_t hmask = S - 1, hshift = 32u - J.log2s;
     bool stop = false;
+    uint32_t nins = 0;                                             // new keys, flushed per block
     // a warp loads the offsets of 32 incident edges at once (lane = edge), then walks them with
     // 128 pins in flight per iteration (4 per lane)
     for (uint64_t kb = i0 + w; kb < i1 && !stop; kb += (uint64_t)NW * 32) {   // round-robin over warps
@@ -79,9 +80,36 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
             const uint32_t idx = b4 + u * 32 + lane;
             m[u] = idx < lj ? __ldg(pj + idx) : n;
           }
+          // first probes of the 4 pins issued back to back (ILP); a hit (the common case: most
+          // pins repeat a neighbour already seen) needs nothing else
+          if constexpr (!SMEM) {   // global-memory table: generic atomics
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (m[u] != n && hs_insert(tab, J.log2s, m[u])) ulist[atomicAdd(&s_cnt, 1u)] = m[u];
+            for (int u = 0; u < 4; ++u)
+              if (m[u] != n && hs_insert(tab, J.log2s, m[u])) ++nins;
+          } else {
+          uint32_t sl[4], kk[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) sl[u] = (m[u] * 0x9E3779B1u) >> hshift;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) kk[u] = lds_u32(tab_s + 4 * sl[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (m[u] == n || kk[u] == m[u]) continue;
+            uint32_t slot = sl[u], k2 = kk[u];
+            while (true) {
+              if (k2 == kEmpty) {
+                k2 = cas_u32(tab_s + 4 * slot, kEmpty, m[u]);
+                if (k2 == kEmpty) { ++nins; break; }
+              }
+              if (k2 == m[u]) break;
+              slot = (slot + 1) & hmask;
+              k2 = lds_u32(tab_s + 4 * slot);
+            }
+          }
+          }
+          const uint32_t tins = __reduce_add_sync(0xFFFFFFFFu, nins);
+          if (lane == 0 && tins) atomicAdd(&s_cnt, tins);
+          nins = 0;
         }
       }
     }
@@ -99,7 +127,20 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
     } else if (s_state == 2) {
       if (tid == 0) J.pool_list[atomicAdd(J.pool_count, 1u)] = n;
     } else {
-      for (uint32_t i = tid; i < count; i += THREADS) J.pool[s_start + i] = ulist[i];   // coalesced
+      // compact the occupied slots: warps sweep 32 consecutive slots at a time (conflict-free)
+      if (tid == 0) s_cnt = 0;
+      __syncthreads();
+      const uint32_t lt = (1u << lane) - 1;
+      for (uint32_t sb = w * 32; sb < S; sb += NW * 32) {
+        const uint32_t v = tab[sb + lane];
+        const bool has = v != kEmpty;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, has);
+        if (!bal) continue;
+        uint32_t wpos = 0;
+        if (lane == 0) wpos = atomicAdd(&s_cnt, __popc(bal));
+        wpos = __shfl_sync(0xFFFFFFFFu, wpos, 0);
+        if (has) J.pool[s_start + wpos + __popc(bal & lt)] = v;
+      }
       if (tid == 0) { J.start[n - J.lo] = s_start; J.cnt[n - J.lo] = count; }
     }
     __syncthreads();
@@ -197,8 +238,8 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
 
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_nbrs<kT1Threads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 << kT1Log);
-    cudaFuncSetAttribute(k_nbrs<kT2Threads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 << kT2Log);
+    cudaFuncSetAttribute(k_nbrs<kT1Threads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT1Log);
+    cudaFuncSetAttribute(k_nbrs<kT2Threads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT2Log);
     attr = true;
   }
   // Run the three tiers with a given pool; returns pool-overflow count and the pool cursor
@@ -215,12 +256,12 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
     J.log2s = kT1Log; J.cap = (1u << (kT1Log - 1)) - 128 * (kT1Threads / 32);
     J.ovf_list = list1; J.ovf_count = counters + 0;
     const uint32_t grid1 = nn < 32u * c->sm_count ? nn : 32u * c->sm_count;
-    HGP_TRY(launch(c, "nbrs_t1", k_nbrs<kT1Threads, true>, dim3(grid1), dim3(kT1Threads), 6u << kT1Log, J));
+    HGP_TRY(launch(c, "nbrs_t1", k_nbrs<kT1Threads, true>, dim3(grid1), dim3(kT1Threads), 4u << kT1Log, J));
     // tier 2: 128 KB shared table for the overflowed nodes (grid-stride over a device count)
     J.list = list1; J.list_count = counters + 0;
     J.log2s = kT2Log; J.cap = (1u << (kT2Log - 1)) - 128 * (kT2Threads / 32);
     J.ovf_list = list2; J.ovf_count = counters + 1;
-    HGP_TRY(launch(c, "nbrs_t2", k_nbrs<kT2Threads, true>, dim3(c->sm_count), dim3(kT2Threads), 6u << kT2Log, J));
+    HGP_TRY(launch(c, "nbrs_t2", k_nbrs<kT2Threads, true>, dim3(c->sm_count), dim3(kT2Threads), 4u << kT2Log, J));
     uint32_t hc[4];
     HGP_TRY(read_back(c, counters, 16, hc));
     if (hc[1]) {   // tier 3: global-memory tables sized from the neighbourhood bound
@@ -232,7 +273,7 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
       uint32_t lg = 1;
       while ((1ull << lg) < 2 * (mb + 1) + 128 * 8) ++lg;
       const uint32_t ctas = hc[1] < (uint32_t)c->sm_count ? hc[1] : (uint32_t)c->sm_count;
-      uint32_t *gtab = scratch_raw<uint32_t>(c, ((size_t)ctas * 3 << lg) / 2, &st);
+      uint32_t *gtab = scratch_raw<uint32_t>(c, (size_t)ctas << lg, &st);
       if (st) return st;
       J.list = list2; J.list_count = counters + 1; J.log2s = lg; J.cap = 0xFFFFFFFFu; J.gtab = gtab;
       J.ovf_list = list1; J.ovf_count = counters + 4;   // cannot overflow: table >= 2 (bound + 1)

@@ -11,102 +11,9 @@
 // bins by (eta + noise desc, id desc) (Eq.6 max_id) become the candidates.
 #include "csr_impl.cuh"
 #include "hashset.cuh"
+#include "score_common.cuh"
 
 namespace hgp {
-
-struct ScoreJob {
-  // level
-  const uint64_t *edge_off;
-  const uint32_t *edge_nsrc, *pins, *edge_w, *edge_mu, *node_w;
-  const uint64_t *inc_off;
-  const uint32_t *inc_nin, *inc, *in_mu;
-  // neighbours
-  uint32_t lo, hi;
-  const uint64_t *nb_off;
-  uint32_t *nbr;
-  // params
-  uint64_t omega, delta, noise_cap, seed_mix;
-  uint32_t pi, norm;
-  hgp_cand *cand;
-  // scheduling
-  const uint32_t *list;        // nodes of this launch (nullptr: every node of [lo,hi))
-  const uint32_t *list_count;
-  uint32_t cap;                // neighbour entries this tier holds (table load <= 1/2)
-  uint32_t log2s;
-  uint32_t *gtab;              // global tables when !SMEM
-  uint32_t *big_list, *big_count;    // deferred: neighbourhood larger than cap
-  uint32_t *wide_list, *wide_count;  // deferred: packed 32-bit accumulator would overflow
-};
-
-enum { kModeP32 = 0, kModeWide = 1 };
-
-template <int PIMAX>
-struct Top {   // best-first list of (score, id); empty entries have id == kNone
-  uint64_t s[PIMAX];
-  uint32_t id[PIMAX];
-};
-
-__device__ __forceinline__ bool better(uint64_t s1, uint32_t i1, uint64_t s2, uint32_t i2) {
-  // (score desc, id desc); an empty entry (kNone) is worse than any real one
-  if (i2 == kNone) return i1 != kNone;
-  if (i1 == kNone) return false;
-  return s1 > s2 || (s1 == s2 && i1 > i2);
-}
-
-template <int PIMAX>
-__device__ __forceinline__ void top_insert(Top<PIMAX> &t, uint32_t pi, uint64_t s, uint32_t id) {
-#pragma unroll
-  for (int i = 0; i < PIMAX; ++i) {
-    if (i < (int)pi && better(s, id, t.s[i], t.id[i])) {
-      uint64_t ts = t.s[i]; uint32_t ti = t.id[i];
-      t.s[i] = s; t.id[i] = id;
-      s = ts; id = ti;
-    }
-  }
-}
-
-// pi rounds: warp argmax of the lanes' list heads; the winner lane pops its head. Lane 0 writes
-// the merged best-first list to out_s/out_id[0..pi).
-template <int PIMAX>
-__device__ __forceinline__ void warp_top_merge(const Top<PIMAX> &top, uint32_t pi, uint64_t *out_s, uint32_t *out_id) {
-  const uint32_t lane = lane_id();
-  uint32_t head = 0;
-  for (uint32_t r = 0; r < pi; ++r) {
-    uint64_t hs = 0;
-    uint32_t hid = kNone;
-#pragma unroll
-    for (int i = 0; i < PIMAX; ++i)
-      if (i == (int)head) { hs = top.s[i]; hid = top.id[i]; }
-    uint32_t who = lane;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t os = __shfl_xor_sync(0xFFFFFFFFu, hs, o);
-      const uint32_t oi = __shfl_xor_sync(0xFFFFFFFFu, hid, o);
-      const uint32_t ow = __shfl_xor_sync(0xFFFFFFFFu, who, o);
-      if (better(os, oi, hs, hid)) { hs = os; hid = oi; who = ow; }
-    }
-    if (lane == 0) { out_s[r] = hs; out_id[r] = hid; }
-    if (hid != kNone && who == lane) ++head;
-  }
-}
-
-__device__ __forceinline__ uint64_t gcd64(uint64_t a, uint64_t b) {
-  if (a == 0) return b;
-  if (b == 0) return a;
-  const int sh = __ffsll((long long)(a | b)) - 1;
-  a >>= __ffsll((long long)a) - 1;
-  do {
-    b >>= __ffsll((long long)b) - 1;
-    if (a > b) { uint64_t t = a; a = b; b = t; }
-    b -= a;
-  } while (b);
-  return a << sh;
-}
-
-__device__ __forceinline__ uint64_t edge_c(const ScoreJob &J, uint32_t e, uint64_t a, uint64_t b) {
-  const uint64_t we = (uint64_t)J.edge_w[e] << HGP_FP_SHIFT;   // Eq.5 term, 2^-24 fixed point
-  return J.norm ? we : we / (b - a);
-}
 
 // One CTA per node. MODE kModeP32: one u32 per bin packs (eta/g) << ib | inter, where g is the
 // gcd of the node's c(e) and ib = bits(in_mu(n)) (exact: inter <= in_mu(n) < 2^ib, and the
@@ -192,7 +99,7 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
     // ---- phase 2: traverse I(n): a warp loads the metadata of 32 incident edges at
     // once (lane = edge), then walks them; pins are fetched 128 at a time (4 per lane in flight).
     // Incident edges are dealt round-robin to warps (edge i0 + w + NW*l, l = 0, 1, ...): balanced.
-    const uint32_t keys_s = smem_u32addr(keys), acc_s = smem_u32addr(acc);
+    const uint32_t keys_s = opaque_u32(smem_u32addr(keys)), acc_s = opaque_u32(smem_u32addr(acc));
     const uint32_t hmask = S - 1, hshift = 32u - log2s;
     for (uint64_t kb = i0 + w; kb < i1; kb += (uint64_t)NW * 32) {
       const uint64_t k = kb + (uint64_t)NW * lane;
@@ -234,20 +141,36 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
             const uint32_t idx = b4 + u * 32 + lane;
             m[u] = idx < lj ? __ldg(pj + idx) : kEmpty;
           }
+          if constexpr (MODE == kModeP32) {
+            // first probes of the 4 pins issued back to back (ILP), collisions resolved after
+            uint32_t sl[4], kk[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sl[u] = (m[u] * 0x9E3779B1u) >> hshift;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) kk[u] = lds_u32(keys_s + 4 * sl[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (m[u] == kEmpty) continue;
+              uint32_t slot = sl[u];
+              if (kk[u] != m[u]) {
+                uint32_t k2 = kk[u];
+                while (true) {
+                  if (k2 == kEmpty) { slot = S; break; }               // purged neighbour -> trash
+                  slot = (slot + 1) & hmask;
+                  k2 = lds_u32(keys_s + 4 * slot);
+                  if (k2 == m[u]) break;
+                }
+              }
+              const bool dst = b4 + u * 32 + lane >= sj;
+              red_add_u32(acc_s + 4 * slot, dst ? ad_j : as_j);
+            }
+            continue;
+          }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (m[u] == kEmpty) continue;
             const bool dst = b4 + u * 32 + lane >= sj;
-            if (MODE == kModeP32) {
-              uint32_t slot = (m[u] * 0x9E3779B1u) >> hshift;
-              while (true) {
-                const uint32_t kk = lds_u32(keys_s + 4 * slot);
-                if (kk == m[u]) break;
-                if (kk == kEmpty) { slot = S; break; }                 // purged neighbour -> trash
-                slot = (slot + 1) & hmask;
-              }
-              red_add_u32(acc_s + 4 * slot, dst ? ad_j : as_j);
-            } else {
+            {
               if (m[u] == n) continue;
               const uint32_t slot = hs_find(keys, log2s, m[u]);
               if (slot == kNone) continue;                          // purged neighbour
@@ -262,7 +185,7 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
     // ---- phase 3: validity (Eq.6), purge flags, noise, per-thread top-pi
     Top<PIMAX> top;
 #pragma unroll
-    for (int i = 0; i < PIMAX; ++i) { top.s[i] = 0; top.id[i] = kNone; }
+    for (int i = 0; i < PIMAX; ++i) { top.s[i] = 0; top.id[i] = 0; }
     const uint64_t wn = J.node_w[n];
     const uint32_t imask = ib ? (uint32_t)((1ull << ib) - 1) : 0u;
     for (uint64_t k = b0 + tid; k < b1; k += THREADS) {
@@ -295,7 +218,7 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
     if (w == 0) {
       Top<PIMAX> t2;
 #pragma unroll
-      for (int i = 0; i < PIMAX; ++i) { t2.s[i] = 0; t2.id[i] = kNone; }
+      for (int i = 0; i < PIMAX; ++i) { t2.s[i] = 0; t2.id[i] = 0; }
       for (uint32_t i = lane; i < NW * J.pi; i += 32) {
         const uint32_t ww = i / J.pi, r = i % J.pi;
         top_insert<PIMAX>(t2, J.pi, s_tops[ww * PIMAX + r], s_topi[ww * PIMAX + r]);
@@ -304,9 +227,9 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
       __syncwarp();
       for (uint32_t r = lane; r < J.pi; r += 32) {
         hgp_cand cd;
-        cd.id = s_topi[NW * PIMAX + r];
+        cd.score = s_tops[NW * PIMAX + r];
+        cd.id = cd.score ? s_topi[NW * PIMAX + r] : kNone;
         cd.pad = 0;
-        cd.score = cd.id == kNone ? 0 : s_tops[NW * PIMAX + r];
         J.cand[(uint64_t)n * J.pi + r] = cd;
       }
     }
@@ -339,7 +262,7 @@ static constexpr uint32_t kSWLog = 12, kSWThreads = 256;
 
 template <int PIMAX>
 hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_deg, uint32_t *lists,
-                              uint32_t *counts) {
+                              uint32_t *counts, const uint32_t *first_list, const uint32_t *first_count) {
   hgp_status st = HGP_OK;
   static bool attr = false;
   if (!attr) {
@@ -353,9 +276,9 @@ hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_
   }
   uint32_t *bigA = lists, *wide = lists + nn, *huge = lists + 2 * (size_t)nn;
   // A: every node; larger neighbourhoods -> bigA, packed overflow -> wide
-  J.list = nullptr; J.list_count = nullptr; J.cap = 1u << (kSALog - 1); J.log2s = kSALog;
+  J.list = first_list; J.list_count = first_count; J.cap = 1u << (kSALog - 1); J.log2s = kSALog;
   J.big_list = bigA; J.big_count = counts + 0; J.wide_list = wide; J.wide_count = counts + 1;
-  const uint32_t gA = nn < 64u * c->sm_count ? nn : 64u * c->sm_count;
+  const uint32_t gA = first_list ? 8u * c->sm_count : (nn < 64u * c->sm_count ? nn : 64u * c->sm_count);
   HGP_TRY(launch(c, "score_A", k_score<kSAThreads, kModeP32, true, PIMAX>, dim3(gA), dim3(kSAThreads), (8u << kSALog) + 16,
                  J));
   if (max_deg > (1u << (kSALog - 1))) {   // B: big neighbourhoods, packed
@@ -385,17 +308,18 @@ hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_
 
 using namespace hgp;
 
-extern "C" hgp_status hgp_score_pairs(hgp_ctx *c, const hgp_csr *g, hgp_nbrs *nb, const hgp_params *p, hgp_cand *cand) {
-  if (!c || !g || !nb || !p || !cand) return set_error(HGP_E_ARG, "hgp_score_pairs: null argument");
+namespace hgp {
+
+// Argument checks, feasibility and the overflow guard shared by a3 and the fused path.
+// Launches k_score_check (errors are read by score_finish).
+hgp_status score_prologue(hgp_ctx *c, const hgp_csr *g, uint32_t lo, uint32_t hi, const hgp_params *p, ScoreJob *J) {
   if (p->pi < 1 || p->pi > HGP_MAX_PI) return set_error(HGP_E_ARG, "pi must be in [1,16]");
   if (p->norm > 1) return set_error(HGP_E_ARG, "norm must be 0 or 1");
   if (p->noise_cap >= (1ull << 56)) return set_error(HGP_E_ARG, "noise_cap >= 2^56");
-  if (nb->hi > g->N || nb->lo > nb->hi) return set_error(HGP_E_ARG, "bad neighbour range");
-  ApiScope scope(c);
+  if (hi > g->N || lo > hi) return set_error(HGP_E_ARG, "bad neighbour range");
   hgp_status st = HGP_OK;
-  const uint32_t lo = nb->lo, hi = nb->hi, nn = hi - lo;
+  const uint32_t nn = hi - lo;
   HGP_TRY(clear_errors(c));
-  uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
   unsigned long long *wsum = scratch_zero<unsigned long long>(c, 1, &st);
   if (st) return st;
   const uint32_t gchk = div_up(nn > g->E ? nn : g->E, 256);
@@ -403,32 +327,28 @@ extern "C" hgp_status hgp_score_pairs(hgp_ctx *c, const hgp_csr *g, hgp_nbrs *nb
                  (const uint32_t *)g->node_w, (const uint32_t *)g->in_mu, lo, hi, p->omega, p->delta,
                  (const uint64_t *)g->edge_off, (const uint32_t *)g->edge_w, g->E, p->norm, c->d_err, wsum));
   // overflow guard (reading #2): matching totals < 2^62
-  {
-    unsigned __int128 tot;
-    if (p->norm) {
-      uint64_t ws = 0;
-      HGP_TRY(read_u64(c, (const uint64_t *)wsum, &ws));
-      tot = (unsigned __int128)ws << HGP_FP_SHIFT;
-    } else {
-      tot = (unsigned __int128)0xFFFFFFFFull << HGP_FP_SHIFT;   // sum omega < 2^32 (a1 guard)
-    }
-    tot += (unsigned __int128)(g->N / 2 + 1) * p->noise_cap;
-    if (tot >= ((unsigned __int128)1 << 62)) return set_error(HGP_E_OVERFLOW, "score totals may exceed 2^62");
+  unsigned __int128 tot;
+  if (p->norm) {
+    uint64_t ws = 0;
+    HGP_TRY(read_u64(c, (const uint64_t *)wsum, &ws));
+    tot = (unsigned __int128)ws << HGP_FP_SHIFT;
+  } else {
+    tot = (unsigned __int128)0xFFFFFFFFull << HGP_FP_SHIFT;   // sum omega < 2^32 (a1 guard)
   }
-  ScoreJob J{};
-  J.edge_off = g->edge_off; J.edge_nsrc = g->edge_nsrc; J.pins = g->pins; J.edge_w = g->edge_w;
-  J.edge_mu = g->edge_mu; J.node_w = g->node_w; J.inc_off = g->inc_off; J.inc_nin = g->inc_nin;
-  J.inc = g->inc; J.in_mu = g->in_mu;
-  J.lo = lo; J.hi = hi; J.nb_off = nb->off; J.nbr = nb->nbr;
-  J.omega = p->omega; J.delta = p->delta; J.noise_cap = p->noise_cap;
-  J.seed_mix = splitmix64_host(p->noise_seed);
-  J.pi = p->pi; J.norm = p->norm; J.cand = cand;
-  uint32_t *lists = scratch_raw<uint32_t>(c, 3 * (size_t)(nn ? nn : 1), &st);
-  if (st) return st;
-  if (nn) {
-    if (p->pi <= 4) HGP_TRY(launch_score_tiers<4>(c, J, nn, nb->max_deg, lists, counts));
-    else HGP_TRY(launch_score_tiers<16>(c, J, nn, nb->max_deg, lists, counts));
-  }
+  tot += (unsigned __int128)(g->N / 2 + 1) * p->noise_cap;
+  if (tot >= ((unsigned __int128)1 << 62)) return set_error(HGP_E_OVERFLOW, "score totals may exceed 2^62");
+  *J = ScoreJob{};
+  J->edge_off = g->edge_off; J->edge_nsrc = g->edge_nsrc; J->pins = g->pins; J->edge_w = g->edge_w;
+  J->edge_mu = g->edge_mu; J->node_w = g->node_w; J->inc_off = g->inc_off; J->inc_nin = g->inc_nin;
+  J->inc = g->inc; J->in_mu = g->in_mu;
+  J->lo = lo; J->hi = hi;
+  J->omega = p->omega; J->delta = p->delta; J->noise_cap = p->noise_cap;
+  J->seed_mix = splitmix64_host(p->noise_seed);
+  J->pi = p->pi; J->norm = p->norm;
+  return HGP_OK;
+}
+
+hgp_status score_finish(hgp_ctx *c) {
   uint64_t err[kErrSlots];
   HGP_TRY(fetch_errors(c, err));
   if (err[kErrInfeasW] != UINT64_MAX || err[kErrInfeasD] != UINT64_MAX) {
@@ -438,4 +358,29 @@ extern "C" hgp_status hgp_score_pairs(hgp_ctx *c, const hgp_csr *g, hgp_nbrs *nb
     return set_error(HGP_E_INFEASIBLE, "node %llu: inbound edges exceed delta", (unsigned long long)b);
   }
   return HGP_OK;
+}
+
+hgp_status score_run(hgp_ctx *c, const hgp_csr *g, hgp_nbrs *nb, const hgp_params *p, hgp_cand *cand,
+                     const uint32_t *list, const uint32_t *list_count) {
+  ScoreJob J;
+  HGP_TRY(score_prologue(c, g, nb->lo, nb->hi, p, &J));
+  hgp_status st = HGP_OK;
+  const uint32_t nn = nb->hi - nb->lo;
+  uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
+  uint32_t *lists = scratch_raw<uint32_t>(c, 3 * (size_t)(nn ? nn : 1), &st);
+  if (st) return st;
+  J.nb_off = nb->off; J.nbr = nb->nbr; J.cand = cand;
+  if (nn) {
+    if (p->pi <= 4) HGP_TRY(launch_score_tiers<4>(c, J, nn, nb->max_deg, lists, counts, list, list_count));
+    else HGP_TRY(launch_score_tiers<16>(c, J, nn, nb->max_deg, lists, counts, list, list_count));
+  }
+  return score_finish(c);
+}
+
+}  // namespace hgp
+
+extern "C" hgp_status hgp_score_pairs(hgp_ctx *c, const hgp_csr *g, hgp_nbrs *nb, const hgp_params *p, hgp_cand *cand) {
+  if (!c || !g || !nb || !p || !cand) return set_error(HGP_E_ARG, "hgp_score_pairs: null argument");
+  ApiScope scope(c);
+  return score_run(c, g, nb, p, cand, nullptr, nullptr);
 }

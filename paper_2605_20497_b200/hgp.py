@@ -118,10 +118,16 @@ def lib():
                                    ctypes.POINTER(CNbrs)]
         L.hgp_coarsen_level.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.POINTER(CNbrs), ctypes.POINTER(CParams), vp,
                                         vp, vp, ctypes.POINTER(CCsr), ctypes.POINTER(CNbrs), ctypes.POINTER(CStats)]
+        L.hgp_neighbors_and_scores.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.POINTER(CParams),
+                                               ctypes.POINTER(CNbrs), vp]
+        L.hgp_coarsen_level0.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.POINTER(CParams), vp, vp, vp,
+                                         ctypes.POINTER(CNbrs), ctypes.POINTER(CCsr), ctypes.POINTER(CNbrs),
+                                         ctypes.POINTER(CStats)]
         L.hgp_csr_free.argtypes = [vp, ctypes.POINTER(CCsr)]
         L.hgp_nbrs_free.argtypes = [vp, ctypes.POINTER(CNbrs)]
         for f in (L.hgp_ctx_create, L.hgp_copy, L.hgp_sync, L.hgp_build_csr, L.hgp_unique_neighbors,
-                  L.hgp_score_pairs, L.hgp_match, L.hgp_contract, L.hgp_coarsen_level):
+                  L.hgp_score_pairs, L.hgp_match, L.hgp_contract, L.hgp_coarsen_level,
+                  L.hgp_neighbors_and_scores, L.hgp_coarsen_level0):
             f.restype = S
         _LIB = L
     return _LIB
@@ -344,6 +350,23 @@ def coarsen_level(ctx: Ctx, g: Csr, nb: Nbrs, p: CParams, cand: torch.Tensor | N
     _check(lib().hgp_coarsen_level(ctx.h, ctypes.byref(g.c), ctypes.byref(nb.c), ctypes.byref(p), _ptr(cand),
                                    _ptr(match_t), _ptr(gamma), ctypes.byref(oc), ctypes.byref(on), ctypes.byref(st)))
     return Csr(ctx, oc), Nbrs(ctx, on), st.as_dict(p.pi)
+
+
+def neighbors_and_scores(ctx: Ctx, g: Csr, p: CParams, cand: torch.Tensor) -> Nbrs:
+    """Fused a2 + a3 on a level without flags (level 0)."""
+    out = CNbrs()
+    _check(lib().hgp_neighbors_and_scores(ctx.h, ctypes.byref(g.c), ctypes.byref(p), ctypes.byref(out), _ptr(cand)))
+    return Nbrs(ctx, out)
+
+
+def coarsen_level0(ctx: Ctx, g: Csr, p: CParams, cand: torch.Tensor | None, match_t: torch.Tensor,
+                   gamma: torch.Tensor):
+    """First level from a level-0 CSR: fused a2+a3, a4, a5. Returns (nb, coarse, coarse_nb, stats)."""
+    nb, oc, on, st = CNbrs(), CCsr(), CNbrs(), CStats()
+    _check(lib().hgp_coarsen_level0(ctx.h, ctypes.byref(g.c), ctypes.byref(p), _ptr(cand), _ptr(match_t),
+                                    _ptr(gamma), ctypes.byref(nb), ctypes.byref(oc), ctypes.byref(on),
+                                    ctypes.byref(st)))
+    return Nbrs(ctx, nb), Csr(ctx, oc), Nbrs(ctx, on), st.as_dict(p.pi)
 
 
 def cand_to_numpy(cand: torch.Tensor) -> np.ndarray:

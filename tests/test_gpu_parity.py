@@ -233,3 +233,38 @@ def test_long_chain_pointer_jumping(hgp, ctx):
     hgp.match(ctx, cand, g.N, 4, m, None)
     rm, _, _ = ref.match(rcand, 4)
     assert np.array_equal(m.cpu().numpy(), rm)
+
+
+FUSED_CASES = [
+    ("snn-small", lambda: hgpgen.snn(5, layers=4, rows=20, cols=20, fanout=30, window=9, rewire=0.1), 16, 256),
+    ("snn-model", lambda: hgpgen.snn(6, layers=3, rows=30, cols=30, fanout=60, window=11), 64, 4096),
+    ("C1", lambda: hgpgen.tiny(1), 16, 32),
+    ("vlsi-small", lambda: hgpgen.vlsi(6, 20000, 20000, dmax=1024, in_cap=600), 64, 600),
+    ("kway", lambda: hgpgen.vlsi(7, 5000, 5000, dmax=200, in_cap=10 ** 6), 2575, hgpgen.UNBOUNDED),
+]
+
+
+@pytest.mark.parametrize("name,make,omega,delta", FUSED_CASES, ids=[c[0] for c in FUSED_CASES])
+def test_fused_level0_matches_oracle(hgp, ctx, name, make, omega, delta):
+    """hgp_coarsen_level0 (fused a2+a3 when representable) == oracle a2, a3, a4, a5."""
+    hg = make()
+    cap = hgpgen.default_noise_cap(hg)
+    g = gpu_build(hgp, ctx, hg)
+    m = torch.empty(g.N, dtype=torch.uint32, device="cuda")
+    gam = torch.empty(g.N, dtype=torch.uint32, device="cuda")
+    cand = hgp.empty_cand(g.N, 4)
+    ctx.profile_begin("nbr")
+    nb, cg, cnb, st = hgp.coarsen_level0(ctx, g, hgp.params(omega, delta, 4, noise_seed=2, noise_cap=cap), cand, m, gam)
+    ctx.profile_end()
+    used = ctx.profile_report()
+    rg = ref.build_csr_hg(hg)
+    rnb = ref.unique_neighbors(rg)
+    rr = ref.coarsen_level(rg, rnb, ref.params(omega, delta, 4, noise_seed=2, noise_cap=cap))
+    assert_nbrs_equal(nb.to_host(), rnb, "fused nbrs+flags")
+    assert_cand_equal(hgp.cand_to_numpy(cand), rr["cand"])
+    assert np.array_equal(m.cpu().numpy(), rr["match"])
+    assert np.array_equal(gam.cpu().numpy(), rr["gamma"])
+    assert_csr_equal(cg.to_host(), rr["coarse"], "fused coarse")
+    assert_nbrs_equal(cnb.to_host(), rr["coarse_nb"], "fused coarse nbrs")
+    if name.startswith("snn"):   # uniform edge weights: the fused kernel handles every node
+        assert "nbrscore_A" in used and "nbrs_t1" not in used, used

@@ -33,8 +33,7 @@ def main():
     gam = torch.empty(N, dtype=torch.uint32, device="cuda")
     for _ in range(a.steps):
         g = hgp.build_csr(ctx, N, dev["edge_off"], dev["edge_nsrc"], dev["pins"], dev["edge_w"], dev["node_w"])
-        nb = hgp.unique_neighbors(ctx, g)
-        cg, cnb, st = hgp.coarsen_level(ctx, g, nb, p, cand, m, gam)
+        nb, cg, cnb, st = hgp.coarsen_level0(ctx, g, p, cand, m, gam)
         print(st, flush=True)
         for x in (g, nb, cg, cnb):
             x.free()
