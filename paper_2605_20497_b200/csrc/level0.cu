@@ -19,10 +19,12 @@
 
 namespace hgp {
 
+constexpr uint32_t kProbeCap = 64;   // longer probe runs mean the table is (nearly) full
+
 struct FusedJob {
   ScoreJob S;                     // level arrays + parameters + cand
   const uint32_t *list, *list_count;   // nodes to process (nullptr: all of [lo, hi))
-  uint32_t log2s, cap;            // table size, max unique neighbours before overflow
+  uint32_t log2s;                 // table size
   uint32_t *pool;
   uint64_t pool_cap;
   unsigned long long *pool_cursor;
@@ -31,13 +33,87 @@ struct FusedJob {
   uint32_t *defer_list, *defer_count;
 };
 
-template <int THREADS, int PIMAX>
-__global__ void __launch_bounds__(THREADS) k_nbrscore(FusedJob F) {
+// Phase 2b + 3 of k_nbrscore. PACKED: every score of the node is < 2^32, so (score, id) is
+// one u64 key (exact order, one compare).
+template <int PIMAX, int THREADS, bool PACKED>
+__device__ __forceinline__ void eval_top(const ScoreJob &J, const FusedJob &F, uint32_t n, uint32_t count,
+                                         const uint32_t *keys, const uint32_t *acc, const uint16_t *ulist, uint64_t g,
+                                         uint32_t ib, uint64_t base, uint64_t *s_tops, uint32_t *s_topi) {
+  constexpr uint32_t NW = THREADS / 32;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  Top<PIMAX> top;
+  TopK<PIMAX> topk;
+#pragma unroll
+  for (int i = 0; i < PIMAX; ++i) { top.s[i] = 0; top.id[i] = 0; topk.k[i] = 0; }
+  const uint64_t wn = J.node_w[n];
+  const uint32_t inn = J.in_mu[n];
+  const uint32_t imask = ib ? (uint32_t)((1ull << ib) - 1) : 0u;
+  for (uint32_t i = tid; i < count; i += THREADS) {
+    const uint32_t slot = ulist[i];
+    const uint32_t v = keys[slot];
+    const uint32_t x = acc[slot];
+    const uint64_t e_nm = (uint64_t)(ib < 32 ? x >> ib : 0) * g;
+    const uint64_t inter = x & imask;
+    const uint64_t uni = (uint64_t)inn + J.in_mu[v] - inter;      // |in(n) ∪ in(m)|
+    const bool ok = wn + J.node_w[v] <= J.omega && (J.delta == HGP_UNBOUNDED || uni <= J.delta);
+    F.pool[base + i] = ok ? v : (v | kPurge);
+    if (!ok) continue;
+    uint64_t sc = e_nm;
+    if (J.noise_cap) {
+      const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
+      sc += __umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);   // uniform in [0, cap]
+    }
+    if (PACKED) topk_insert<PIMAX>(topk, J.pi, (sc << 32) | v);
+    else top_insert<PIMAX>(top, J.pi, sc, v);
+  }
+  if (PACKED) warp_topk_merge<PIMAX>(topk, J.pi, s_tops + w * PIMAX);
+  else warp_top_merge<PIMAX>(top, J.pi, s_tops + w * PIMAX, s_topi + w * PIMAX);
+  __syncthreads();
+  if (w == 0) {
+    if (PACKED) {
+      TopK<PIMAX> t2;
+#pragma unroll
+      for (int i = 0; i < PIMAX; ++i) t2.k[i] = 0;
+      for (uint32_t i = lane; i < NW * J.pi; i += 32) topk_insert<PIMAX>(t2, J.pi, s_tops[(i / J.pi) * PIMAX + i % J.pi]);
+      warp_topk_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX);
+      __syncwarp();
+      for (uint32_t r = lane; r < J.pi; r += 32) {
+        const uint64_t k = s_tops[NW * PIMAX + r];
+        hgp_cand cd;
+        cd.score = k >> 32;
+        cd.id = k ? (uint32_t)k : kNone;
+        cd.pad = 0;
+        J.cand[(uint64_t)n * J.pi + r] = cd;
+      }
+    } else {
+      Top<PIMAX> t2;
+#pragma unroll
+      for (int i = 0; i < PIMAX; ++i) { t2.s[i] = 0; t2.id[i] = 0; }
+      for (uint32_t i = lane; i < NW * J.pi; i += 32) {
+        const uint32_t ww = i / J.pi, r = i % J.pi;
+        top_insert<PIMAX>(t2, J.pi, s_tops[ww * PIMAX + r], s_topi[ww * PIMAX + r]);
+      }
+      warp_top_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX, s_topi + NW * PIMAX);
+      __syncwarp();
+      for (uint32_t r = lane; r < J.pi; r += 32) {
+        hgp_cand cd;
+        cd.score = s_tops[NW * PIMAX + r];
+        cd.id = cd.score ? s_topi[NW * PIMAX + r] : kNone;
+        cd.pad = 0;
+        J.cand[(uint64_t)n * J.pi + r] = cd;
+      }
+    }
+  }
+}
+
+template <int THREADS, int PIMAX, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ uint64_t s_tops[(THREADS / 32 + 1) * PIMAX];
   __shared__ uint32_t s_topi[(THREADS / 32 + 1) * PIMAX];
   __shared__ uint64_t s_sum[THREADS / 32], s_g[THREADS / 32];
-  __shared__ uint32_t s_defer, s_cnt, s_ib, s_count;
+  __shared__ uint32_t s_defer, s_ib, s_count, s_small;
+  __shared__ uint32_t s_wcnt[THREADS / 32];
   __shared__ uint64_t s_gcd;
   __shared__ unsigned long long s_start;
   constexpr uint32_t NW = THREADS / 32;
@@ -46,10 +122,9 @@ __global__ void __launch_bounds__(THREADS) k_nbrscore(FusedJob F) {
   const uint32_t log2s = F.log2s, S = 1u << log2s;
   uint32_t *keys = reinterpret_cast<uint32_t *>(dyn);
   uint32_t *acc = keys + S;
-  uint32_t *ulist = acc + S;                                      // dense list of neighbour slots
+  uint16_t *ulist = reinterpret_cast<uint16_t *>(acc + S);        // dense list of neighbour slots (S <= 65536)
   const uint32_t keys_s = opaque_u32(smem_u32addr(keys)), acc_s = opaque_u32(smem_u32addr(acc));
   const uint32_t hmask = S - 1, hshift = 32u - log2s;
-  volatile uint32_t *vcnt = &s_cnt;
   const uint32_t total = F.list_count ? *F.list_count : J.hi - J.lo;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = F.list ? F.list[t] : J.lo + t;
@@ -84,7 +159,7 @@ __global__ void __launch_bounds__(THREADS) k_nbrscore(FusedJob F) {
       s_defer = need > ((unsigned __int128)1 << 32);
       s_gcd = G1;
       s_ib = bits;
-      s_cnt = 0;
+      s_small = (unsigned __int128)S1 + J.noise_cap < ((unsigned __int128)1 << 32);
       hs_insert(keys, log2s, n);                                 // self-visits land in n's slot
     }
     __syncthreads();
@@ -96,10 +171,9 @@ __global__ void __launch_bounds__(THREADS) k_nbrscore(FusedJob F) {
     const uint64_t g = s_gcd;
     const uint32_t ib = s_ib;
     // ---- phase 1 (= a2 + a3 traversal): insert-or-find every pin, add its packed term.
-    // New keys are counted per lane and flushed once per 128-pin block (warp reduce + one
-    // shared atomic) so that the overflow vote sees a count lagging by < 128 per warp.
+    // No counter in the hot loop: a probe sequence longer than kProbeCap means the table is
+    // (nearly) full, and the node goes to the next tier (results of a deferred node are unused).
     bool stop = false;
-    uint32_t nins = 0;
     for (uint64_t kb = i0 + w; kb < i1 && !stop; kb += (uint64_t)NW * 32) {
       const uint64_t k = kb + (uint64_t)NW * lane;
       uint64_t a = 0;
@@ -122,7 +196,6 @@ __global__ void __launch_bounds__(THREADS) k_nbrscore(FusedJob F) {
         const uint32_t ad_j = __shfl_sync(0xFFFFFFFFu, add_d, j);
         const uint32_t *pj = J.pins + aj;
         for (uint32_t b4 = 0; b4 < lj; b4 += 128) {
-          if (__any_sync(0xFFFFFFFFu, *vcnt >= F.cap)) { stop = true; break; }   // warp-uniform vote
           uint32_t m[4], sl[4], kk[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -133,107 +206,77 @@ __global__ void __launch_bounds__(THREADS) k_nbrscore(FusedJob F) {
           for (int u = 0; u < 4; ++u) sl[u] = (m[u] * 0x9E3779B1u) >> hshift;
 #pragma unroll
           for (int u = 0; u < 4; ++u) kk[u] = lds_u32(keys_s + 4 * sl[u]);
+          bool full = false;
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (m[u] == kEmpty) continue;
-            uint32_t slot = sl[u], k2 = kk[u];
+            uint32_t slot = sl[u], k2 = kk[u], probes = 0;
             while (k2 != m[u]) {
               if (k2 == kEmpty) {
                 k2 = cas_u32(keys_s + 4 * slot, kEmpty, m[u]);
-                if (k2 == kEmpty) { ++nins; break; }
+                if (k2 == kEmpty) break;
                 continue;                                           // re-test the winner's key
               }
+              if (++probes > kProbeCap) { full = true; break; }
               slot = (slot + 1) & hmask;
               k2 = lds_u32(keys_s + 4 * slot);
             }
-            red_add_u32(acc_s + 4 * slot, b4 + u * 32 + lane >= sj ? ad_j : as_j);
+            if (!full) red_add_u32(acc_s + 4 * slot, b4 + u * 32 + lane >= sj ? ad_j : as_j);
           }
-          const uint32_t tins = __reduce_add_sync(0xFFFFFFFFu, nins);
-          if (lane == 0 && tins) atomicAdd(&s_cnt, tins);
-          nins = 0;
+          if (__any_sync(0xFFFFFFFFu, full)) { stop = true; break; }
         }
       }
     }
     if (stop && lane == 0) s_defer = 1;
     __syncthreads();
-    if (tid == 0) {
-      const uint32_t c0 = s_cnt;
-      s_count = c0;
-      if (!s_defer) {
-        const unsigned long long st = atomicAdd(F.pool_cursor, (unsigned long long)c0);
-        s_start = st;
-        if (st + c0 > F.pool_cap) s_defer = 1;
-      }
-      s_cnt = 0;                                                  // reused as the compaction cursor
-    }
-    __syncthreads();
-    const uint32_t count = s_count;
     if (s_defer) {
       if (tid == 0) F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
       __syncthreads();
       continue;
     }
-    // ---- phase 2a: compact the occupied slots (but n's) into a dense list: warps sweep 32
-    // consecutive slots at a time (conflict-free) with a ballot and one shared atomic per chunk
+    // ---- phase 2a: compact the occupied slots (but n's) into a dense list. Each warp owns a
+    // contiguous range of the table: pass 1 counts (ballots), a warp-level prefix gives offsets,
+    // pass 2 writes — no atomics, conflict-free 32-slot sweeps.
     const uint32_t lt = (1u << lane) - 1;
-    for (uint32_t sb = w * 32; sb < S; sb += NW * 32) {
+    const uint32_t per_w = S / NW, w0 = w * per_w;
+    uint32_t mine = 0;
+    for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
+      const uint32_t v = keys[sb + lane];
+      mine += __popc(__ballot_sync(0xFFFFFFFFu, v != kEmpty && v != n));
+    }
+    if (lane == 0) s_wcnt[w] = mine;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t acc0 = 0;
+      for (uint32_t q = 0; q < NW; ++q) { const uint32_t c1 = s_wcnt[q]; s_wcnt[q] = acc0; acc0 += c1; }
+      s_count = acc0;
+      if (acc0 > S / 2) {                                         // the dense list holds S/2 entries
+        s_defer = 1;
+        F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
+      } else {
+        const unsigned long long st = atomicAdd(F.pool_cursor, (unsigned long long)acc0);
+        s_start = st;
+        if (st + acc0 > F.pool_cap) { s_defer = 1; F.defer_list[atomicAdd(F.defer_count, 1u)] = n; }
+      }
+    }
+    __syncthreads();
+    if (s_defer) { __syncthreads(); continue; }
+    uint32_t wpos = s_wcnt[w];
+    for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
       const uint32_t v = keys[sb + lane];
       const bool has = v != kEmpty && v != n;
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, has);
-      if (!bal) continue;
-      uint32_t wpos = 0;
-      if (lane == 0) wpos = atomicAdd(&s_cnt, __popc(bal));
-      wpos = __shfl_sync(0xFFFFFFFFu, wpos, 0);
       if (has) ulist[wpos + __popc(bal & lt)] = sb + lane;
+      wpos += __popc(bal);
     }
     __syncthreads();
+    const uint32_t count = s_count;
     // ---- phase 2b: validity (Eq.6), flags, the N(n) entries with their flags,
-    // noise, per-thread top-pi
-    Top<PIMAX> top;
-#pragma unroll
-    for (int i = 0; i < PIMAX; ++i) { top.s[i] = 0; top.id[i] = 0; }
-    const uint64_t wn = J.node_w[n];
-    const uint32_t imask = ib ? (uint32_t)((1ull << ib) - 1) : 0u;
-    const uint64_t base = s_start;
-    for (uint32_t i = tid; i < count; i += THREADS) {
-      const uint32_t slot = ulist[i];
-      const uint32_t v = keys[slot];
-      const uint32_t x = acc[slot];
-      const uint64_t e_nm = (uint64_t)(ib < 32 ? x >> ib : 0) * g;
-      const uint64_t inter = x & imask;
-      const uint64_t uni = (uint64_t)inn + J.in_mu[v] - inter;    // |in(n) ∪ in(m)|
-      const bool ok = wn + J.node_w[v] <= J.omega && (J.delta == HGP_UNBOUNDED || uni <= J.delta);
-      F.pool[base + i] = ok ? v : (v | kPurge);
-      if (!ok) continue;
-      uint64_t sc = e_nm;
-      if (J.noise_cap) {
-        const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
-        sc += __umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);   // uniform in [0, cap]
-      }
-      top_insert<PIMAX>(top, J.pi, sc, v);
-    }
-    if (tid == 0) { F.start[n - J.lo] = base; F.cnt[n - J.lo] = count; }
-    // ---- phase 3: top-pi merge (warps, then warp 0)
-    warp_top_merge<PIMAX>(top, J.pi, s_tops + w * PIMAX, s_topi + w * PIMAX);
-    __syncthreads();
-    if (w == 0) {
-      Top<PIMAX> t2;
-#pragma unroll
-      for (int i = 0; i < PIMAX; ++i) { t2.s[i] = 0; t2.id[i] = 0; }
-      for (uint32_t i = lane; i < NW * J.pi; i += 32) {
-        const uint32_t ww = i / J.pi, r = i % J.pi;
-        top_insert<PIMAX>(t2, J.pi, s_tops[ww * PIMAX + r], s_topi[ww * PIMAX + r]);
-      }
-      warp_top_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX, s_topi + NW * PIMAX);
-      __syncwarp();
-      for (uint32_t r = lane; r < J.pi; r += 32) {
-        hgp_cand cd;
-        cd.score = s_tops[NW * PIMAX + r];
-        cd.id = cd.score ? s_topi[NW * PIMAX + r] : kNone;
-        cd.pad = 0;
-        J.cand[(uint64_t)n * J.pi + r] = cd;
-      }
-    }
+    // noise, per-thread top-pi; phase 3: top-pi merge (warps, then warp 0)
+    if (tid == 0) F.start[n - J.lo] = s_start;
+    if (tid == 0) F.cnt[n - J.lo] = count;
+    if (s_small) eval_top<PIMAX, THREADS, true>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
+    else eval_top<PIMAX, THREADS, false>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
     __syncthreads();
   }
 }
@@ -268,33 +311,32 @@ __global__ void k_pairs_total(const uint64_t *edge_off, uint32_t E, unsigned lon
 static constexpr uint32_t kFALog = 12, kFAThreads = 128;
 static constexpr uint32_t kFBLog = 14, kFBThreads = 256;
 
-template <int PIMAX, int TA>
+template <int PIMAX, int TA, int MINB>
 hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, uint32_t nn, uint32_t *lists, uint32_t *counts) {
   static bool attr = false;
+  constexpr uint32_t smemA = (8u << kFALog) + (2u << (kFALog - 1)), smemB = (8u << kFBLog) + (2u << (kFBLog - 1));
   if (!attr) {
-    cudaFuncSetAttribute(k_nbrscore<TA, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 10 << kFALog);
-    cudaFuncSetAttribute(k_nbrscore<kFBThreads, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 10 << kFBLog);
+    cudaFuncSetAttribute(k_nbrscore<TA, PIMAX, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemA);
+    cudaFuncSetAttribute(k_nbrscore<kFBThreads, PIMAX, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemB);
     attr = true;
   }
   F.list = nullptr; F.list_count = nullptr; F.log2s = kFALog;
-  F.cap = (1u << (kFALog - 1)) - 128 * (TA / 32) - 1;
   F.defer_list = lists; F.defer_count = counts + 0;
   const uint32_t per_sm = TA == 128 ? 32u : 16u;
   const uint32_t gA = nn < per_sm * c->sm_count ? nn : per_sm * c->sm_count;
-  HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX>, dim3(gA), dim3(TA), 10u << kFALog, F));
+  HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB>, dim3(gA), dim3(TA), smemA, F));
   F.list = lists; F.list_count = counts + 0; F.log2s = kFBLog;
-  F.cap = (1u << (kFBLog - 1)) - 128 * (kFBThreads / 32) - 1;
   F.defer_list = lists + nn; F.defer_count = counts + 1;
-  HGP_TRY(launch(c, "nbrscore_B", k_nbrscore<kFBThreads, PIMAX>, dim3(c->sm_count), dim3(kFBThreads),
-                 10u << kFBLog, F));
+  HGP_TRY(launch(c, "nbrscore_B", k_nbrscore<kFBThreads, PIMAX, 1>, dim3(c->sm_count), dim3(kFBThreads), smemB, F));
   return HGP_OK;
 }
 
 template <int PIMAX>
 hgp_status fused_tiers(hgp_ctx *c, FusedJob F, uint32_t nn, uint32_t *lists, uint32_t *counts) {
-  static const int threads = getenv("HGP_FUSED_THREADS") ? atoi(getenv("HGP_FUSED_THREADS")) : 256;
-  if (threads == 128) return fused_tiers_t<PIMAX, 128>(c, F, nn, lists, counts);
-  return fused_tiers_t<PIMAX, 256>(c, F, nn, lists, counts);
+  static const int cfg = getenv("HGP_FUSED_CFG") ? atoi(getenv("HGP_FUSED_CFG")) : 1;
+  if (cfg == 1) return fused_tiers_t<PIMAX, 256, 6>(c, F, nn, lists, counts);
+  if (cfg == 2) return fused_tiers_t<PIMAX, 256, 4>(c, F, nn, lists, counts);
+  return fused_tiers_t<PIMAX, 256, 5>(c, F, nn, lists, counts);
 }
 
 // a2 + a3 on a level-0 CSR (no flags yet). Returns the same nb and cand as hgp_unique_neighbors

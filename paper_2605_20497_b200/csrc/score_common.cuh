@@ -79,6 +79,46 @@ __device__ __forceinline__ void warp_top_merge(const Top<PIMAX> &top, uint32_t p
   }
 }
 
+// Packed keys (score << 32 | id) when every score of the node is < 2^32: one u64 compare orders
+// (score desc, id desc) exactly. Empty entries are 0 (every real score >= 1).
+template <int PIMAX>
+struct TopK {
+  uint64_t k[PIMAX];
+};
+
+template <int PIMAX>
+__device__ __forceinline__ void topk_insert(TopK<PIMAX> &t, uint32_t pi, uint64_t key) {
+#pragma unroll
+  for (int i = 0; i < PIMAX; ++i) {
+    if (i < (int)pi && key > t.k[i]) {
+      const uint64_t x = t.k[i];
+      t.k[i] = key;
+      key = x;
+    }
+  }
+}
+
+// pi rounds of warp argmax over the lanes' list heads (keys are distinct unless empty).
+template <int PIMAX>
+__device__ __forceinline__ void warp_topk_merge(const TopK<PIMAX> &top, uint32_t pi, uint64_t *out) {
+  const uint32_t lane = lane_id();
+  uint32_t head = 0;
+  for (uint32_t r = 0; r < pi; ++r) {
+    uint64_t h = 0;
+#pragma unroll
+    for (int i = 0; i < PIMAX; ++i)
+      if (i == (int)head) h = top.k[i];
+    uint64_t best = h;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t ob = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+      best = ob > best ? ob : best;
+    }
+    if (lane == 0) out[r] = best;
+    if (best != 0 && h == best) ++head;
+  }
+}
+
 __device__ __forceinline__ uint64_t gcd64(uint64_t a, uint64_t b) {
   if (a == 0) return b;
   if (b == 0) return a;
