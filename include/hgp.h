@@ -191,13 +191,19 @@ HGP_API hgp_status hgp_coarsen_level(hgp_ctx *ctx, const hgp_csr *g, hgp_nbrs *n
                                      hgp_cand *cand, uint32_t *match, uint32_t *gamma, hgp_csr *coarse,
                                      hgp_nbrs *coarse_nb, hgp_level_stats *stats);
 
-/* a2 + a3 fused for a level whose neighbour lists carry no flags yet (the first level): one
- * traversal of I(n) builds N(n) and its histogram together (see level0.cu). Outputs are
- * identical to hgp_unique_neighbors(g, 0, N) followed by hgp_score_pairs; nodes the fused
- * kernel cannot represent make the call run that unfused pair instead. nb is allocated by
- * the library (all nodes); cand is caller [N][pi]. Synchronises. */
-HGP_API hgp_status hgp_neighbors_and_scores(hgp_ctx *ctx, const hgp_csr *g, const hgp_params *p, hgp_nbrs *nb,
-                                           hgp_cand *cand);
+/* a2 + a3 fused for nodes [lo, hi) of a level whose neighbour lists carry no flags yet (the
+ * first level): one traversal of I(n) builds N(n) and its histogram together (level0.cu).
+ * Outputs are identical to hgp_unique_neighbors(g, lo, hi) followed by hgp_score_pairs; nodes
+ * the fused kernel cannot represent make the call run that unfused pair instead. nb (covering
+ * lo..hi) is allocated by the library; cand is caller [N][pi], rows lo..hi-1 written.
+ * Synchronises. */
+HGP_API hgp_status hgp_neighbors_and_scores(hgp_ctx *ctx, const hgp_csr *g, const hgp_params *p, uint32_t lo,
+                                           uint32_t hi, hgp_nbrs *nb, hgp_cand *cand);
+
+/* Node-range sharding for multi-GPU (north_star: "scoring and matching shard by node range over
+ * a replicated CSR"): bounds[0..world] (HOST) splits [0, N) into contiguous ranges of about equal
+ * traversal work sum_{e in I(n)} |e|. Deterministic (depends on the replicated CSR only). */
+HGP_API hgp_status hgp_shard_bounds(hgp_ctx *ctx, const hgp_csr *g, uint32_t world, uint32_t *bounds);
 
 /* The first level straight from a level-0 CSR: fused a2+a3 -> a4 -> a5. nb receives N(n) with
  * the purge flags set by a3 (library-owned). cand may be NULL; stats (HOST) may be NULL. */

@@ -7,5 +7,6 @@ namespace hgp {
 hgp_status build_incidence(hgp_ctx *c, hgp_csr *g);
 void free_csr(hgp_ctx *c, hgp_csr *g);
 void free_nbrs(hgp_ctx *c, hgp_nbrs *nb);
-hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, hgp_nbrs *out, hgp_cand *cand);
+hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, uint32_t lo, uint32_t hi,
+                            hgp_nbrs *out, hgp_cand *cand);
 }  // namespace hgp

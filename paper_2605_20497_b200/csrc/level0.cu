@@ -341,11 +341,12 @@ hgp_status fused_tiers(hgp_ctx *c, FusedJob F, uint32_t nn, uint32_t *lists, uin
 
 // a2 + a3 on a level-0 CSR (no flags yet). Returns the same nb and cand as hgp_unique_neighbors
 // followed by hgp_score_pairs. Synchronises.
-hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, hgp_nbrs *out, hgp_cand *cand) {
+hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, uint32_t lo, uint32_t hi,
+                            hgp_nbrs *out, hgp_cand *cand) {
   memset(out, 0, sizeof(*out));
-  const uint32_t nn = g->N;
+  const uint32_t nn = hi - lo;
   ScoreJob J;
-  HGP_TRY(score_prologue(c, g, 0, nn, p, &J));
+  HGP_TRY(score_prologue(c, g, lo, hi, p, &J));
   J.cand = cand;
   hgp_status st = HGP_OK;
   unsigned long long *misc = scratch_zero<unsigned long long>(c, 2, &st);    // T, pool cursor
@@ -359,7 +360,9 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, h
                  dim3(256), 0, (const uint64_t *)g->edge_off, g->E, misc));
   uint64_t T = 0;
   HGP_TRY(read_u64(c, (const uint64_t *)misc, &T));
-  uint64_t pool_cap = T < 24 * g->P + nn ? T : 24 * g->P + nn;
+  // pool estimate: min(T, 24 P) scaled to the range (nodes that do not fit make the call fall back)
+  const double frac = g->N ? (double)nn / g->N : 1.0;
+  uint64_t pool_cap = (uint64_t)((T < 24 * g->P ? T : 24 * g->P) * (frac < 1.0 ? 1.25 * frac : 1.0)) + nn;
   if (pool_cap == 0) pool_cap = 1;
   uint32_t *pool = scratch_raw<uint32_t>(c, pool_cap, &st);
   if (st) return st;
@@ -372,8 +375,8 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, h
   HGP_TRY(read_back(c, counts, 8, hc));
   if (hc[1]) return HGP_E_INTERNAL;      // some node needs the unfused path: caller falls back
   HGP_TRY(score_finish(c));
-  out->lo = 0;
-  out->hi = nn;
+  out->lo = lo;
+  out->hi = hi;
   out->off = dalloc_n<uint64_t>(c, (size_t)nn + 1, &st);
   if (st) return st;
   uint64_t V = 0;
@@ -398,19 +401,65 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
 
 using namespace hgp;
 
-extern "C" hgp_status hgp_neighbors_and_scores(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, hgp_nbrs *nb,
-                                               hgp_cand *cand) {
+extern "C" hgp_status hgp_neighbors_and_scores(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, uint32_t lo,
+                                               uint32_t hi, hgp_nbrs *nb, hgp_cand *cand) {
   if (!c || !g || !p || !nb || !cand) return set_error(HGP_E_ARG, "hgp_neighbors_and_scores: null argument");
+  if (lo > hi || hi > g->N) return set_error(HGP_E_ARG, "hgp_neighbors_and_scores: bad node range");
   ApiScope scope(c);
-  hgp_status s = g->N ? nbrs_score_fused(c, g, p, nb, cand) : HGP_E_INTERNAL;
+  hgp_status s = hi > lo ? nbrs_score_fused(c, g, p, lo, hi, nb, cand) : HGP_E_INTERNAL;
   if (s == HGP_OK) return HGP_OK;
   if (s != HGP_E_INTERNAL) { free_nbrs(c, nb); return s; }
   // unfused path: a2 then a3 (identical results)
   free_nbrs(c, nb);
-  HGP_TRY(hgp_unique_neighbors(c, g, 0, g->N, nb));
+  HGP_TRY(hgp_unique_neighbors(c, g, lo, hi, nb));
   s = score_run(c, g, nb, p, cand, nullptr, nullptr);
   if (s != HGP_OK) free_nbrs(c, nb);
   return s;
+}
+
+__global__ void k_node_work(const uint64_t *inc_off, const uint32_t *inc, const uint64_t *edge_off, uint32_t N,
+                            uint64_t *work) {
+  const uint32_t lane = lane_id();
+  for (uint32_t n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < N; n += gridDim.x * (blockDim.x >> 5)) {
+    uint64_t s = 0;
+    for (uint64_t k = inc_off[n] + lane; k < inc_off[n + 1]; k += 32) {
+      const uint32_t e = inc[k];
+      s += edge_off[e + 1] - edge_off[e];
+    }
+    s = warp_sum(s);
+    if (lane == 0) work[n] = s + 1;                              // +1: every node costs something
+  }
+}
+
+__global__ void k_split(const uint64_t *prefix, uint32_t N, uint32_t world, uint32_t *bounds) {
+  const uint32_t r = threadIdx.x;
+  if (r > world) return;
+  if (r == 0) { bounds[0] = 0; return; }
+  if (r == world) { bounds[world] = N; return; }
+  const uint64_t target = (prefix[N] * r + world - 1) / world;
+  uint32_t a = 0, b = N;                                          // first n with prefix[n] >= target
+  while (a < b) {
+    const uint32_t mid = (a + b) >> 1;
+    if (prefix[mid] < target) a = mid + 1; else b = mid;
+  }
+  bounds[r] = a;
+}
+
+extern "C" hgp_status hgp_shard_bounds(hgp_ctx *c, const hgp_csr *g, uint32_t world, uint32_t *bounds) {
+  if (!c || !g || !bounds || world == 0 || world > 1024) return set_error(HGP_E_ARG, "hgp_shard_bounds: bad argument");
+  ApiScope scope(c);
+  hgp_status st = HGP_OK;
+  const uint32_t N = g->N;
+  uint64_t *work = scratch_raw<uint64_t>(c, N ? N : 1, &st);
+  uint64_t *prefix = scratch_raw<uint64_t>(c, (size_t)N + 1, &st);
+  uint32_t *db = scratch_raw<uint32_t>(c, world + 1, &st);
+  if (st) return st;
+  const uint32_t grid = N ? (div_up(N, 8) < 16u * c->sm_count ? div_up(N, 8) : 16u * c->sm_count) : 0;
+  HGP_TRY(launch(c, "node_work", k_node_work, dim3(grid), dim3(256), 0, (const uint64_t *)g->inc_off,
+                 (const uint32_t *)g->inc, (const uint64_t *)g->edge_off, N, work));
+  HGP_TRY(scan_exclusive(c, InU64{work}, N, prefix, nullptr));
+  HGP_TRY(launch(c, "split", k_split, dim3(1), dim3(world + 1), 0, (const uint64_t *)prefix, N, world, db));
+  return read_back(c, db, 4 * ((size_t)world + 1), bounds);
 }
 
 extern "C" hgp_status hgp_coarsen_level0(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, hgp_cand *cand,
@@ -428,7 +477,7 @@ extern "C" hgp_status hgp_coarsen_level0(hgp_ctx *c, const hgp_csr *g, const hgp
   uint32_t *per = scratch_zero<uint32_t>(c, HGP_MAX_PI, &st);
   if (st) return st;
   HGP_CUDA(cudaEventRecord(c->ev[0], c->stream));
-  HGP_TRY(hgp_neighbors_and_scores(c, g, p, nb, cand));
+  HGP_TRY(hgp_neighbors_and_scores(c, g, p, 0, g->N, nb, cand));
   HGP_CUDA(cudaEventRecord(c->ev[1], c->stream));
   hgp_status s = hgp_match(c, cand, g->N, p->pi, match, per);
   if (s != HGP_OK) { free_nbrs(c, nb); return s; }

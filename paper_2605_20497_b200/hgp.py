@@ -118,8 +118,10 @@ def lib():
                                    ctypes.POINTER(CNbrs)]
         L.hgp_coarsen_level.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.POINTER(CNbrs), ctypes.POINTER(CParams), vp,
                                         vp, vp, ctypes.POINTER(CCsr), ctypes.POINTER(CNbrs), ctypes.POINTER(CStats)]
-        L.hgp_neighbors_and_scores.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.POINTER(CParams),
-                                               ctypes.POINTER(CNbrs), vp]
+        L.hgp_neighbors_and_scores.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.POINTER(CParams), ctypes.c_uint32,
+                                               ctypes.c_uint32, ctypes.POINTER(CNbrs), vp]
+        L.hgp_shard_bounds.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32)]
+        L.hgp_shard_bounds.restype = S
         L.hgp_coarsen_level0.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.POINTER(CParams), vp, vp, vp,
                                          ctypes.POINTER(CNbrs), ctypes.POINTER(CCsr), ctypes.POINTER(CNbrs),
                                          ctypes.POINTER(CStats)]
@@ -352,11 +354,20 @@ def coarsen_level(ctx: Ctx, g: Csr, nb: Nbrs, p: CParams, cand: torch.Tensor | N
     return Csr(ctx, oc), Nbrs(ctx, on), st.as_dict(p.pi)
 
 
-def neighbors_and_scores(ctx: Ctx, g: Csr, p: CParams, cand: torch.Tensor) -> Nbrs:
-    """Fused a2 + a3 on a level without flags (level 0)."""
+def neighbors_and_scores(ctx: Ctx, g: Csr, p: CParams, cand: torch.Tensor, lo: int = 0, hi: int | None = None) -> Nbrs:
+    """Fused a2 + a3 on nodes [lo, hi) of a level without flags (level 0)."""
+    hi = g.N if hi is None else hi
     out = CNbrs()
-    _check(lib().hgp_neighbors_and_scores(ctx.h, ctypes.byref(g.c), ctypes.byref(p), ctypes.byref(out), _ptr(cand)))
+    _check(lib().hgp_neighbors_and_scores(ctx.h, ctypes.byref(g.c), ctypes.byref(p), lo, hi, ctypes.byref(out),
+                                          _ptr(cand)))
     return Nbrs(ctx, out)
+
+
+def shard_bounds(ctx: Ctx, g: Csr, world: int) -> list[int]:
+    """[0 = b_0 <= b_1 <= ... <= b_world = N]: equal-work contiguous node ranges."""
+    arr = (ctypes.c_uint32 * (world + 1))()
+    _check(lib().hgp_shard_bounds(ctx.h, ctypes.byref(g.c), world, arr))
+    return list(arr)
 
 
 def coarsen_level0(ctx: Ctx, g: Csr, p: CParams, cand: torch.Tensor | None, match_t: torch.Tensor,
