@@ -238,15 +238,16 @@ def main():
 
     def step(inp):
         g = hgp.build_csr(ctx, N, inp["edge_off"], inp["edge_nsrc"], inp["pins"], inp["edge_w"], inp["node_w"])
-        if world == 1:
-            nb, cg, cnb, st = hgp.coarsen_level0(ctx, g, params, cand, match, gamma)
+        if world == 1:   # N(n) is consumed by a5 where the fused kernel left it (not returned)
+            nb, cg, cnb, st = hgp.coarsen_level0(ctx, g, params, cand, match, gamma, want_nbrs=False)
         else:   # node-range shards of a2+a3, NCCL all-gathers, replicated a4 + a5 (shard.py)
             nb, cg, cnb, info = shard.level0_sharded(ctx, g, params, cand, match, gamma)
-            st = {"Nc": cg.N, "Ec": cg.E, "Pc": cg.P, "Vc": cnb.V, "matched_per_round": [], "purged": 0,
+            st = {"Nc": cg.N, "Ec": cg.E, "Pc": cg.P, "Vc": cnb.V, "V": nb.V, "matched_per_round": [], "purged": 0,
                   "merged_edges": 0, "dropped_edges": 0}
-        last.update(st=st, V=nb.V, max_deg=nb.c.max_deg)
+        last.update(st=st, V=nb.V if nb is not None else st["V"])
         for x in (g, nb, cg, cnb):
-            x.free()
+            if x is not None:
+                x.free()
 
     def barrier():
         if world > 1:

@@ -206,7 +206,9 @@ HGP_API hgp_status hgp_neighbors_and_scores(hgp_ctx *ctx, const hgp_csr *g, cons
 HGP_API hgp_status hgp_shard_bounds(hgp_ctx *ctx, const hgp_csr *g, uint32_t world, uint32_t *bounds);
 
 /* The first level straight from a level-0 CSR: fused a2+a3 -> a4 -> a5. nb receives N(n) with
- * the purge flags set by a3 (library-owned). cand may be NULL; stats (HOST) may be NULL. */
+ * the purge flags set by a3 (library-owned); nb may be NULL, in which case N(n) is consumed by a5
+ * where the fused kernel left it (no compaction pass) and not returned. cand may be NULL;
+ * stats (HOST) may be NULL. */
 HGP_API hgp_status hgp_coarsen_level0(hgp_ctx *ctx, const hgp_csr *g, const hgp_params *p, hgp_cand *cand,
                                       uint32_t *match, uint32_t *gamma, hgp_nbrs *nb, hgp_csr *coarse,
                                       hgp_nbrs *coarse_nb, hgp_level_stats *stats);

@@ -207,7 +207,9 @@ __global__ void k_coarse_edge_pack(const uint32_t *rep, const uint64_t *ceid, co
 // ---------------------------------------------------------------- coarse neighbours
 struct CNbrJob {
   const uint32_t *mem0, *mem1;
-  const uint64_t *nb_off;
+  const uint64_t *nb_off;      // CSR offsets, or nullptr when nb_start/nb_len describe the segments
+  const uint64_t *nb_start;
+  const uint32_t *nb_len;
   const uint32_t *nbr;
   const uint32_t *gamma;
   const uint64_t *bound_off;   // exclusive scan of |N(a)|+|N(b)| (oversized slots)
@@ -257,8 +259,14 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t c = J.list ? J.list[t] : t;
     const uint32_t a = J.mem0[c], b = J.mem1[c];
-    const uint64_t a0 = J.nb_off[a], a1 = J.nb_off[a + 1];
-    const uint64_t b0 = b == kNone ? 0 : J.nb_off[b], b1 = b == kNone ? 0 : J.nb_off[b + 1];
+    uint64_t a0, a1, b0 = 0, b1 = 0;
+    if (J.nb_off) {
+      a0 = J.nb_off[a]; a1 = J.nb_off[a + 1];
+      if (b != kNone) { b0 = J.nb_off[b]; b1 = J.nb_off[b + 1]; }
+    } else {
+      a0 = J.nb_start[a]; a1 = a0 + J.nb_len[a];
+      if (b != kNone) { b0 = J.nb_start[b]; b1 = b0 + J.nb_len[b]; }
+    }
     const uint64_t na = a1 - a0, nbn = b1 - b0;
     if (!J.list && na + nbn > J.cap) continue;                      // larger tier (uniform)
     for (uint32_t i = tid; i < S / 4; i += THREADS)
@@ -302,9 +310,11 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
 struct BoundIn {   // |N(a)| + |N(b)| per coarse node
   const uint32_t *mem0, *mem1;
   const uint64_t *nb_off;
+  const uint32_t *nb_len;
+  __device__ uint64_t len(uint32_t n) const { return nb_off ? nb_off[n + 1] - nb_off[n] : nb_len[n]; }
   __device__ uint64_t operator()(uint64_t c) const {
     const uint32_t a = mem0[c], b = mem1[c];
-    return (nb_off[a + 1] - nb_off[a]) + (b == kNone ? 0 : nb_off[b + 1] - nb_off[b]);
+    return len(a) + (b == kNone ? 0 : len(b));
   }
 };
 
@@ -348,7 +358,7 @@ static constexpr uint32_t kCALog = 12, kCAThreads = 128;   // 4096 slots + list:
 static constexpr uint32_t kCBLog = 15, kCBThreads = 256;   // 32768 slots + list: 192 KB, <= 16384 entries
 
 hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match, uint32_t *gamma,
-                         hgp_csr *C, hgp_nbrs *CN, hgp_level_stats *stats) {
+                         hgp_csr *C, hgp_nbrs *CN, hgp_level_stats *stats, const SegView *view) {
   hgp_status st = HGP_OK;
   const uint32_t N = g->N, E = g->E;
   const uint64_t P = g->P;
@@ -441,7 +451,8 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   uint64_t *bound_off = scratch_raw<uint64_t>(c, (size_t)Nc + 1, &st);
   if (st) return st;
   uint64_t Vb = 0;
-  HGP_TRY(scan_exclusive(c, BoundIn{mem0, mem1, nb->off}, Nc, bound_off, &Vb));
+  const uint64_t *seg_off = view ? nullptr : nb->off;
+  HGP_TRY(scan_exclusive(c, BoundIn{mem0, mem1, seg_off, view ? view->len : nullptr}, Nc, bound_off, &Vb));
   uint32_t *pool = scratch_raw<uint32_t>(c, Vb, &st);
   uint32_t *ccnt = scratch_raw<uint32_t>(c, Nc, &st);
   uint32_t *lists = scratch_raw<uint32_t>(c, 2 * (size_t)Nc, &st);
@@ -455,7 +466,9 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
     attr = true;
   }
   CNbrJob J{};
-  J.mem0 = mem0; J.mem1 = mem1; J.nb_off = nb->off; J.nbr = nb->nbr; J.gamma = gamma; J.bound_off = bound_off;
+  J.mem0 = mem0; J.mem1 = mem1; J.nb_off = seg_off; J.gamma = gamma; J.bound_off = bound_off;
+  J.nb_start = view ? view->start : nullptr; J.nb_len = view ? view->len : nullptr;
+  J.nbr = view ? view->nbr : nb->nbr;
   J.pool = pool; J.cnt = ccnt; J.Nc = Nc; J.purged = misc;
   const uint32_t capA = 1u << (kCALog - 1), capB = 1u << (kCBLog - 1);
   J.list = nullptr; J.list_count = nullptr; J.cap = capA; J.log2s = kCALog;
@@ -523,7 +536,7 @@ extern "C" hgp_status hgp_contract(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs 
     return set_error(HGP_E_ARG, "hgp_contract: null argument");
   if (nb->lo != 0 || nb->hi != g->N) return set_error(HGP_E_ARG, "contract needs neighbours of every node");
   ApiScope scope(c);
-  hgp_status s = contract_impl(c, g, nb, match, gamma, coarse, coarse_nb, nullptr);
+  hgp_status s = contract_impl(c, g, nb, match, gamma, coarse, coarse_nb, nullptr, nullptr);
   if (s != HGP_OK) { free_csr(c, coarse); free_nbrs(c, coarse_nb); }
   return s;
 }

@@ -7,6 +7,16 @@ namespace hgp {
 hgp_status build_incidence(hgp_ctx *c, hgp_csr *g);
 void free_csr(hgp_ctx *c, hgp_csr *g);
 void free_nbrs(hgp_ctx *c, hgp_nbrs *nb);
+// Neighbour segments left in the fused kernel's pool (not compacted into a CSR): segment n is
+// nbr[start[n] .. start[n] + len[n]) (scratch of the current top-level call).
+struct SegView {
+  const uint64_t *start;
+  const uint32_t *len;
+  const uint32_t *nbr;
+  uint64_t V;
+};
 hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, uint32_t lo, uint32_t hi,
-                            hgp_nbrs *out, hgp_cand *cand);
+                            hgp_nbrs *out, hgp_cand *cand, SegView *view);
+hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match, uint32_t *gamma,
+                         hgp_csr *C, hgp_nbrs *CN, hgp_level_stats *stats, const SegView *view);
 }  // namespace hgp

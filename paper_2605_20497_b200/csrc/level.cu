@@ -2,10 +2,6 @@
 // with per-step device times from CUDA events on the ctx stream.
 #include "csr_impl.cuh"
 
-namespace hgp {
-hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match, uint32_t *gamma,
-                         hgp_csr *C, hgp_nbrs *CN, hgp_level_stats *stats);
-}
 
 using namespace hgp;
 
@@ -29,7 +25,7 @@ extern "C" hgp_status hgp_coarsen_level(hgp_ctx *c, const hgp_csr *g, hgp_nbrs *
   HGP_CUDA(cudaEventRecord(c->ev[1], c->stream));
   HGP_TRY(hgp_match(c, cand, g->N, p->pi, match, per));
   HGP_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  hgp_status s = contract_impl(c, g, nb, match, gamma, coarse, coarse_nb, stats);
+  hgp_status s = contract_impl(c, g, nb, match, gamma, coarse, coarse_nb, stats, nullptr);
   if (s != HGP_OK) { free_csr(c, coarse); free_nbrs(c, coarse_nb); return s; }
   HGP_CUDA(cudaEventRecord(c->ev[3], c->stream));
   HGP_CUDA(cudaEventSynchronize(c->ev[3]));

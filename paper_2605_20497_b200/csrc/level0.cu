@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
             m[u] = idx < lj ? __ldg(pj + idx) : kEmpty;
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) sl[u] = (m[u] * 0x9E3779B1u) >> hshift;
+          for (int u = 0; u < 4; ++u) sl[u] = hash_slot(m[u], log2s);
 #pragma unroll
           for (int u = 0; u < 4; ++u) kk[u] = lds_u32(keys_s + 4 * sl[u]);
           bool full = false;
@@ -342,8 +342,8 @@ hgp_status fused_tiers(hgp_ctx *c, FusedJob F, uint32_t nn, uint32_t *lists, uin
 // a2 + a3 on a level-0 CSR (no flags yet). Returns the same nb and cand as hgp_unique_neighbors
 // followed by hgp_score_pairs. Synchronises.
 hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, uint32_t lo, uint32_t hi,
-                            hgp_nbrs *out, hgp_cand *cand) {
-  memset(out, 0, sizeof(*out));
+                            hgp_nbrs *out, hgp_cand *cand, SegView *view) {
+  if (out) memset(out, 0, sizeof(*out));
   const uint32_t nn = hi - lo;
   ScoreJob J;
   HGP_TRY(score_prologue(c, g, lo, hi, p, &J));
@@ -375,6 +375,12 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   HGP_TRY(read_back(c, counts, 8, hc));
   if (hc[1]) return HGP_E_INTERNAL;      // some node needs the unfused path: caller falls back
   HGP_TRY(score_finish(c));
+  if (!out) {   // leave N(n) in the pool: segment n = pool[start[n] .. + cnt[n]) (relative to lo)
+    uint64_t V = 0;
+    HGP_TRY(read_u64(c, (const uint64_t *)(misc + 1), &V));
+    view->start = start; view->len = cnt; view->nbr = pool; view->V = V;
+    return HGP_OK;
+  }
   out->lo = lo;
   out->hi = hi;
   out->off = dalloc_n<uint64_t>(c, (size_t)nn + 1, &st);
@@ -394,8 +400,6 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   return HGP_OK;
 }
 
-hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match, uint32_t *gamma,
-                         hgp_csr *C, hgp_nbrs *CN, hgp_level_stats *stats);
 
 }  // namespace hgp
 
@@ -406,7 +410,7 @@ extern "C" hgp_status hgp_neighbors_and_scores(hgp_ctx *c, const hgp_csr *g, con
   if (!c || !g || !p || !nb || !cand) return set_error(HGP_E_ARG, "hgp_neighbors_and_scores: null argument");
   if (lo > hi || hi > g->N) return set_error(HGP_E_ARG, "hgp_neighbors_and_scores: bad node range");
   ApiScope scope(c);
-  hgp_status s = hi > lo ? nbrs_score_fused(c, g, p, lo, hi, nb, cand) : HGP_E_INTERNAL;
+  hgp_status s = hi > lo ? nbrs_score_fused(c, g, p, lo, hi, nb, cand, nullptr) : HGP_E_INTERNAL;
   if (s == HGP_OK) return HGP_OK;
   if (s != HGP_E_INTERNAL) { free_nbrs(c, nb); return s; }
   // unfused path: a2 then a3 (identical results)
@@ -465,7 +469,7 @@ extern "C" hgp_status hgp_shard_bounds(hgp_ctx *c, const hgp_csr *g, uint32_t wo
 extern "C" hgp_status hgp_coarsen_level0(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, hgp_cand *cand,
                                          uint32_t *match, uint32_t *gamma, hgp_nbrs *nb, hgp_csr *coarse,
                                          hgp_nbrs *coarse_nb, hgp_level_stats *stats) {
-  if (!c || !g || !p || !match || !gamma || !nb || !coarse || !coarse_nb)
+  if (!c || !g || !p || !match || !gamma || !coarse || !coarse_nb)
     return set_error(HGP_E_ARG, "hgp_coarsen_level0: null argument");
   if (p->pi < 1 || p->pi > HGP_MAX_PI) return set_error(HGP_E_ARG, "pi must be in [1,16]");
   ApiScope scope(c);
@@ -476,18 +480,30 @@ extern "C" hgp_status hgp_coarsen_level0(hgp_ctx *c, const hgp_csr *g, const hgp
   }
   uint32_t *per = scratch_zero<uint32_t>(c, HGP_MAX_PI, &st);
   if (st) return st;
+  // nb == NULL: the level's N(n) stays in the fused kernel's pool and a5 reads it there (no
+  // compaction pass); otherwise it is returned as a CSR with the flags a3 set.
+  hgp_nbrs local{};
+  hgp_nbrs *use = nb ? nb : &local;
+  SegView view{};
+  bool have_view = false;
   HGP_CUDA(cudaEventRecord(c->ev[0], c->stream));
-  HGP_TRY(hgp_neighbors_and_scores(c, g, p, 0, g->N, nb, cand));
+  if (!nb && g->N) {
+    hgp_status s = nbrs_score_fused(c, g, p, 0, g->N, nullptr, cand, &view);
+    if (s == HGP_OK) have_view = true;
+    else if (s != HGP_E_INTERNAL) return s;
+  }
+  if (!have_view) HGP_TRY(hgp_neighbors_and_scores(c, g, p, 0, g->N, use, cand));
   HGP_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  auto cleanup = [&]() { if (!have_view && !nb) free_nbrs(c, &local); };
   hgp_status s = hgp_match(c, cand, g->N, p->pi, match, per);
-  if (s != HGP_OK) { free_nbrs(c, nb); return s; }
+  if (s != HGP_OK) { cleanup(); if (nb) free_nbrs(c, nb); return s; }
   HGP_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  s = contract_impl(c, g, nb, match, gamma, coarse, coarse_nb, stats);
-  if (s != HGP_OK) { free_csr(c, coarse); free_nbrs(c, coarse_nb); free_nbrs(c, nb); return s; }
+  s = contract_impl(c, g, have_view ? nullptr : use, match, gamma, coarse, coarse_nb, stats, have_view ? &view : nullptr);
+  if (s != HGP_OK) { free_csr(c, coarse); free_nbrs(c, coarse_nb); cleanup(); if (nb) free_nbrs(c, nb); return s; }
   HGP_CUDA(cudaEventRecord(c->ev[3], c->stream));
   HGP_CUDA(cudaEventSynchronize(c->ev[3]));
   if (stats) {
-    stats->N = g->N; stats->E = g->E; stats->P = g->P; stats->V = nb->V;
+    stats->N = g->N; stats->E = g->E; stats->P = g->P; stats->V = have_view ? view.V : use->V;
     uint32_t hper[HGP_MAX_PI];
     HGP_TRY(read_back(c, per, sizeof(hper), hper));
     for (int i = 0; i < HGP_MAX_PI; ++i) stats->matched_per_round[i] = i < (int)p->pi ? hper[i] : 0;
@@ -496,5 +512,6 @@ extern "C" hgp_status hgp_coarsen_level0(hgp_ctx *c, const hgp_csr *g, const hgp
     cudaEventElapsedTime(&stats->ms[2], c->ev[2], c->ev[3]);
     cudaEventElapsedTime(&stats->ms[3], c->ev[0], c->ev[3]);
   }
+  cleanup();
   return HGP_OK;
 }

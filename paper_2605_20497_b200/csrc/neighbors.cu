@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
           } else {
           uint32_t sl[4], kk[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) sl[u] = (m[u] * 0x9E3779B1u) >> hshift;
+          for (int u = 0; u < 4; ++u) sl[u] = hash_slot(m[u], J.log2s);
 #pragma unroll
           for (int u = 0; u < 4; ++u) kk[u] = lds_u32(tab_s + 4 * sl[u]);
 #pragma unroll

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
             // first probes of the 4 pins issued back to back (ILP), collisions resolved after
             uint32_t sl[4], kk[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) sl[u] = (m[u] * 0x9E3779B1u) >> hshift;
+            for (int u = 0; u < 4; ++u) sl[u] = hash_slot(m[u], log2s);
 #pragma unroll
             for (int u = 0; u < 4; ++u) kk[u] = lds_u32(keys_s + 4 * sl[u]);
 #pragma unroll

@@ -33,6 +33,41 @@ __device__ __forceinline__ uint32_t warp_bitonic32(uint32_t key) {
   return key;
 }
 
+// Sort up to 128 keys held 4 per lane (element index i*32 + lane); padding must be 0xFFFFFFFF.
+// Classic bitonic network: stages with j >= 32 pair registers of the same lane, j < 32 pair lanes.
+__device__ __forceinline__ void warp_bitonic128(uint32_t (&v)[4]) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (uint32_t k = 2; k <= 128; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const uint32_t d = j >> 5;
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i) {
+          if (i & d) continue;
+          const uint32_t x = i * 32 + lane;                 // lower index of the pair (i, i|d)
+          const bool up = (x & k) == 0;
+          const uint32_t a = v[i], b = v[i | d];
+          const uint32_t mn = min(a, b), mx = max(a, b);
+          v[i] = up ? mn : mx;
+          v[i | d] = up ? mx : mn;
+        }
+      } else {
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i) {
+          const uint32_t x = i * 32 + lane;
+          const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, v[i], j);
+          const bool up = (x & k) == 0;
+          const bool lower = (lane & j) == 0;
+          const uint32_t mn = min(v[i], other), mx = max(v[i], other);
+          v[i] = (lower == up) ? mn : mx;
+        }
+      }
+    }
+  }
+}
+
 // Sort s[0..n) ascending with nthreads cooperating threads (index tid); SYNC is the barrier.
 template <class Sync>
 __device__ __forceinline__ void bitonic_sort_flip(uint32_t *s, uint32_t n, uint32_t tid, uint32_t nthreads,
@@ -83,6 +118,14 @@ k_segsort_warp(Seg seg, uint64_t nseg, uint32_t *keys, uint64_t *big, uint32_t *
       uint32_t v = lane < len ? k[lane] : 0xFFFFFFFFu;
       v = warp_bitonic32(v);
       if (lane < len) k[lane] = v;
+    } else if (len <= 128) {
+      uint32_t v[4];
+#pragma unroll
+      for (uint32_t i = 0; i < 4; ++i) v[i] = i * 32 + lane < len ? k[i * 32 + lane] : 0xFFFFFFFFu;
+      warp_bitonic128(v);
+#pragma unroll
+      for (uint32_t i = 0; i < 4; ++i)
+        if (i * 32 + lane < len) k[i * 32 + lane] = v[i];
     } else if (len <= kWarpSortCap) {
       uint32_t *s = buf[w];
       for (uint32_t j = lane; j < len; j += 32) s[j] = k[j];

@@ -371,13 +371,14 @@ def shard_bounds(ctx: Ctx, g: Csr, world: int) -> list[int]:
 
 
 def coarsen_level0(ctx: Ctx, g: Csr, p: CParams, cand: torch.Tensor | None, match_t: torch.Tensor,
-                   gamma: torch.Tensor):
-    """First level from a level-0 CSR: fused a2+a3, a4, a5. Returns (nb, coarse, coarse_nb, stats)."""
+                   gamma: torch.Tensor, want_nbrs: bool = True):
+    """First level from a level-0 CSR: fused a2+a3, a4, a5. Returns (nb, coarse, coarse_nb, stats);
+    nb is None when want_nbrs is False (N(n) is then consumed in place by a5)."""
     nb, oc, on, st = CNbrs(), CCsr(), CNbrs(), CStats()
     _check(lib().hgp_coarsen_level0(ctx.h, ctypes.byref(g.c), ctypes.byref(p), _ptr(cand), _ptr(match_t),
-                                    _ptr(gamma), ctypes.byref(nb), ctypes.byref(oc), ctypes.byref(on),
-                                    ctypes.byref(st)))
-    return Nbrs(ctx, nb), Csr(ctx, oc), Nbrs(ctx, on), st.as_dict(p.pi)
+                                    _ptr(gamma), ctypes.byref(nb) if want_nbrs else None, ctypes.byref(oc),
+                                    ctypes.byref(on), ctypes.byref(st)))
+    return (Nbrs(ctx, nb) if want_nbrs else None), Csr(ctx, oc), Nbrs(ctx, on), st.as_dict(p.pi)
 
 
 def cand_to_numpy(cand: torch.Tensor) -> np.ndarray:

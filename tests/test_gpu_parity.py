@@ -268,3 +268,13 @@ def test_fused_level0_matches_oracle(hgp, ctx, name, make, omega, delta):
     assert_nbrs_equal(cnb.to_host(), rr["coarse_nb"], "fused coarse nbrs")
     if name.startswith("snn"):   # uniform edge weights: the fused kernel handles every node
         assert "nbrscore_A" in used and "nbrs_t1" not in used, used
+    # without returning N(n) (a5 reads it from the fused kernel's pool): same level
+    m2 = torch.empty(g.N, dtype=torch.uint32, device="cuda")
+    gam2 = torch.empty(g.N, dtype=torch.uint32, device="cuda")
+    cand2 = hgp.empty_cand(g.N, 4)
+    nb2, cg2, cnb2, st2 = hgp.coarsen_level0(ctx, g, hgp.params(omega, delta, 4, noise_seed=2, noise_cap=cap), cand2,
+                                             m2, gam2, want_nbrs=False)
+    assert nb2 is None and st2["V"] == rnb.nbr.shape[0]
+    assert np.array_equal(m2.cpu().numpy(), rr["match"]) and np.array_equal(gam2.cpu().numpy(), rr["gamma"])
+    assert_csr_equal(cg2.to_host(), rr["coarse"], "fused coarse (pool view)")
+    assert_nbrs_equal(cnb2.to_host(), rr["coarse_nb"], "fused coarse nbrs (pool view)")
