@@ -49,7 +49,8 @@ struct hgp_ctx {
   // scratch arena (reset at every top-level API call)
   struct Chunk { void *p; size_t bytes; };
   std::vector<Chunk> chunks;
-  size_t used = 0;       // bytes used in chunks.back()
+  size_t cur = 0;        // chunk currently bump-allocated from
+  size_t used = 0;       // bytes used in chunks[cur]
   int depth = 0;
   uint64_t launches = 0;
   uint64_t *d_err = nullptr;       // [kErrSlots] device

@@ -246,14 +246,19 @@ __device__ __forceinline__ bool hs_insert_flagged(uint32_t *keys, uint32_t log2s
   }
 }
 
+// One CTA per coarse node c = {a, b}: gamma(N(a) ∪ N(b)) into a hash set whose slots carry an
+// OR-ed purge flag in bit 31; then the unflagged keys other than c are compacted (two ballot
+// passes over the table, warp-owned ranges, no atomics) into c's oversized pool slot.
 template <int THREADS, bool SMEM>
 __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
   extern __shared__ uint32_t dyn[];
-  __shared__ uint32_t s_cnt, s_out;
-  const uint32_t tid = threadIdx.x;
-  const uint32_t S = 1u << J.log2s;
-  uint32_t *keys = SMEM ? dyn : J.gtab + (size_t)blockIdx.x * (((size_t)3 << J.log2s) >> 1);
-  uint32_t *slots = keys + S;                                       // append list of inserted slots
+  constexpr uint32_t NW = THREADS / 32;
+  __shared__ uint32_t s_wcnt[NW];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t log2s = J.log2s, S = 1u << log2s;
+  uint32_t *keys = SMEM ? dyn : J.gtab + ((size_t)blockIdx.x << log2s);
+  const uint32_t keys_s = SMEM ? opaque_u32(smem_u32addr(keys)) : 0u;
+  const uint32_t hmask = S - 1;
   const uint32_t total = J.list_count ? *J.list_count : J.Nc;
   uint64_t purged = 0;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
@@ -271,7 +276,6 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
     if (!J.list && na + nbn > J.cap) continue;                      // larger tier (uniform)
     for (uint32_t i = tid; i < S / 4; i += THREADS)
       reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-    if (tid == 0) { s_cnt = 0; s_out = 0; }
     __syncthreads();
     // 4 entries per thread in flight: nbr loads, then the gamma gathers, then the inserts
     for (uint64_t k0 = tid; k0 < na + nbn; k0 += 4 * THREADS) {
@@ -286,22 +290,51 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (v[u] == kEmpty) continue;
-        uint32_t slot;
         const bool fl = (v[u] & kPurge) != 0;
-        if (hs_insert_flagged(keys, J.log2s, gm[u], fl, &slot)) slots[atomicAdd(&s_cnt, 1u)] = slot;
         purged += fl;
+        if constexpr (SMEM) {
+          uint32_t slot = hash_slot(gm[u], log2s);
+          uint32_t k = lds_u32(keys_s + 4 * slot);
+          while (true) {
+            if (k == kEmpty) {
+              k = cas_u32(keys_s + 4 * slot, kEmpty, fl ? (gm[u] | kPurge) : gm[u]);
+              if (k == kEmpty) break;
+            }
+            if ((k & kIdMask) == gm[u]) {
+              if (fl && !(k & kPurge)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(keys_s + 4 * slot), "r"(kPurge) : "memory");
+              break;
+            }
+            slot = (slot + 1) & hmask;
+            k = lds_u32(keys_s + 4 * slot);
+          }
+        } else {
+          uint32_t slot;
+          hs_insert_flagged(keys, log2s, gm[u], fl, &slot);
+        }
       }
     }
     __syncthreads();
-    const uint32_t nk = s_cnt;
-    uint64_t *dummy = nullptr;
-    (void)dummy;
-    for (uint32_t i = tid; i < nk; i += THREADS) {
-      const uint32_t k = keys[slots[i]];
-      if (!(k & kPurge) && k != c) J.pool[J.bound_off[c] + atomicAdd(&s_out, 1u)] = k;
+    // compact: unflagged keys != c
+    const uint32_t per_w = S / NW, w0 = w * per_w, lt = (1u << lane) - 1;
+    uint32_t mine = 0;
+    for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
+      const uint32_t k = keys[sb + lane];
+      mine += __popc(__ballot_sync(0xFFFFFFFFu, !(k & kPurge) && k != c));   // kEmpty has bit 31 set
     }
+    if (lane == 0) s_wcnt[w] = mine;
     __syncthreads();
-    if (tid == 0) J.cnt[c] = s_out;
+    uint32_t wpos = 0, tot = 0;
+    for (uint32_t q = 0; q < NW; ++q) { const uint32_t x = s_wcnt[q]; if (q < w) wpos += x; tot += x; }
+    const uint64_t base = J.bound_off[c];
+    for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
+      const uint32_t k = keys[sb + lane];
+      const bool keep = !(k & kPurge) && k != c;
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+      if (keep) J.pool[base + wpos + __popc(bal & lt)] = k;
+      wpos += __popc(bal);
+    }
+    if (tid == 0) J.cnt[c] = tot;
+    __syncthreads();
   }
   purged = warp_sum(purged);
   if ((tid & 31) == 0 && purged) atomicAdd(J.purged, (unsigned long long)purged);
@@ -354,8 +387,8 @@ __global__ void k_count_kept(const uint32_t *rep, uint32_t E, uint32_t *out) {
   if (lane_id() == 0 && s) atomicAdd(out, s);
 }
 
-static constexpr uint32_t kCALog = 12, kCAThreads = 128;   // 4096 slots + list: 24 KB, <= 2048 entries
-static constexpr uint32_t kCBLog = 15, kCBThreads = 256;   // 32768 slots + list: 192 KB, <= 16384 entries
+static constexpr uint32_t kCALog = 12, kCAThreads = 256;   // 4096 slots: 16 KB, <= 2048 entries
+static constexpr uint32_t kCBLog = 15, kCBThreads = 256;   // 32768 slots: 128 KB, <= 16384 entries
 
 hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match, uint32_t *gamma,
                          hgp_csr *C, hgp_nbrs *CN, hgp_level_stats *stats, const SegView *view) {
@@ -461,8 +494,8 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   if (st) return st;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_coarse_nbrs<kCAThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 << kCALog);
-    cudaFuncSetAttribute(k_coarse_nbrs<kCBThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 << kCBLog);
+    cudaFuncSetAttribute(k_coarse_nbrs<kCAThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kCALog);
+    cudaFuncSetAttribute(k_coarse_nbrs<kCBThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kCBLog);
     attr = true;
   }
   CNbrJob J{};
@@ -473,7 +506,7 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   const uint32_t capA = 1u << (kCALog - 1), capB = 1u << (kCBLog - 1);
   J.list = nullptr; J.list_count = nullptr; J.cap = capA; J.log2s = kCALog;
   const uint32_t gA = Nc < 64u * c->sm_count ? (Nc ? Nc : 1) : 64u * c->sm_count;
-  HGP_TRY(launch(c, "coarse_nbrs_A", k_coarse_nbrs<kCAThreads, true>, dim3(gA), dim3(kCAThreads), 6u << kCALog, J));
+  HGP_TRY(launch(c, "coarse_nbrs_A", k_coarse_nbrs<kCAThreads, true>, dim3(gA), dim3(kCAThreads), 4u << kCALog, J));
   HGP_TRY(launch(c, "cnbr_classify", k_cnbr_classify, dim3(grid_for(Nc)), dim3(256), 0, (const uint64_t *)bound_off, Nc,
                  capA, capB, lists, lists + Nc, counts, misc + 1));
   uint32_t hc[2];
@@ -481,7 +514,7 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   if (hc[0]) {
     J.list = lists; J.list_count = counts; J.cap = capB; J.log2s = kCBLog;
     HGP_TRY(launch(c, "coarse_nbrs_B", k_coarse_nbrs<kCBThreads, true>, dim3(c->sm_count), dim3(kCBThreads),
-                   6u << kCBLog, J));
+                   4u << kCBLog, J));
   }
   if (hc[1]) {
     uint64_t mb = 0;
@@ -489,7 +522,7 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
     uint32_t lg = kCBLog;
     while ((1ull << (lg - 1)) < mb) ++lg;
     const uint32_t ctas = hc[1] < (uint32_t)c->sm_count ? hc[1] : (uint32_t)c->sm_count;
-    uint32_t *gtab = scratch_raw<uint32_t>(c, ((size_t)ctas * 3 << lg) / 2, &st);
+    uint32_t *gtab = scratch_raw<uint32_t>(c, (size_t)ctas << lg, &st);
     if (st) return st;
     J.list = lists + Nc; J.list_count = counts + 1; J.cap = 0xFFFFFFFFu; J.log2s = lg; J.gtab = gtab;
     HGP_TRY(launch(c, "coarse_nbrs_C", k_coarse_nbrs<256, false>, dim3(ctas), dim3(256), 0, J));

@@ -77,34 +77,42 @@ cudaEvent_t hgp_ctx::prof_event() {
 }
 
 void hgp_ctx::reset_scratch() {
-  if (chunks.size() > 1) {       // consolidate into one chunk of the total size
-    size_t total = 0;
-    for (auto &ch : chunks) { total += ch.bytes; dfree(ch.p, ch.bytes); }
+  // keep only the largest chunk (the steady-state working set of one call fits in it after the
+  // first few calls); smaller ones go back to the allocator
+  if (chunks.size() > 1) {
+    size_t best = 0;
+    for (size_t i = 1; i < chunks.size(); ++i)
+      if (chunks[i].bytes > chunks[best].bytes) best = i;
+    for (size_t i = 0; i < chunks.size(); ++i)
+      if (i != best) dfree(chunks[i].p, chunks[i].bytes);
+    Chunk keep = chunks[best];
     chunks.clear();
-    void *p = dalloc(total);
-    if (p) chunks.push_back({p, total});
+    chunks.push_back(keep);
   }
+  cur = 0;
   used = 0;
 }
 
 void *hgp_ctx::scratch(size_t bytes) {
   bytes = (bytes + 255) & ~size_t(255);
   if (bytes == 0) bytes = 256;
-  if (!chunks.empty() && used + bytes <= chunks.back().bytes) {
-    void *p = static_cast<char *>(chunks.back().p) + used;
-    used += bytes;
-    return p;
+  // first fit in the current chunk, then in later chunks; otherwise a new chunk of exactly the
+  // request (at least 64 MB)
+  while (cur < chunks.size()) {
+    if (used + bytes <= chunks[cur].bytes) {
+      void *p = static_cast<char *>(chunks[cur].p) + used;
+      used += bytes;
+      return p;
+    }
+    if (cur + 1 == chunks.size()) break;
+    ++cur;
+    used = 0;
   }
-  size_t last = chunks.empty() ? 0 : chunks.back().bytes;
-  size_t want = bytes > 2 * last ? bytes : 2 * last;
-  if (want < (size_t(64) << 20)) want = size_t(64) << 20;
+  size_t want = bytes < (size_t(64) << 20) ? (size_t(64) << 20) : bytes;
   void *p = dalloc(want);
-  if (!p) {                       // retry with the exact size
-    want = bytes;
-    p = dalloc(want);
-    if (!p) return nullptr;
-  }
+  if (!p) return nullptr;
   chunks.push_back({p, want});
+  cur = chunks.size() - 1;
   used = bytes;
   return p;
 }

@@ -199,6 +199,78 @@ void free_nbrs(hgp_ctx *c, hgp_nbrs *nb) {
 static constexpr uint32_t kT1Log = 12, kT1Threads = 128;   // 16 KB table + 8 KB list, <= 1536 uniques
 static constexpr uint32_t kT2Log = 15, kT2Threads = 256;   // 128 KB table + 64 KB list
 
+__global__ void k_list_bound_sum(const uint64_t *inc_off, const uint32_t *inc, const uint64_t *edge_off,
+                                 const uint32_t *list, const uint32_t *count, uint32_t N, unsigned long long *sum,
+                                 unsigned long long *mx) {
+  const uint32_t total = *count;
+  uint64_t acc = 0, m = 0;
+  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < total; t += gridDim.x * (blockDim.x >> 5)) {
+    const uint32_t n = list[t];
+    uint64_t s = 0;
+    for (uint64_t k = inc_off[n] + lane_id(); k < inc_off[n + 1]; k += 32) {
+      const uint32_t e = inc[k];
+      s += edge_off[e + 1] - edge_off[e] - 1;
+    }
+    s = warp_sum(s);
+    if (s > N - 1) s = N - 1;
+    acc += s;
+    m = s > m ? s : m;
+  }
+  if (lane_id() == 0) { atomicAdd(sum, (unsigned long long)acc); atomicMax(mx, (unsigned long long)m); }
+}
+
+static constexpr uint32_t kT1LogL = 12, kT1ThreadsL = 128;
+static constexpr uint32_t kT2LogL = 15, kT2ThreadsL = 256;
+
+// a2 for the nodes of a device list (hcount = its host-known length): N(n) into a pool sized by
+// the exact bound sum_n min(sum_{e in I(n)} (|e|-1), N-1), so nothing can overflow.
+// start/cnt are indexed n - lo; *pool_out is scratch of the current call.
+hgp_status nbrs_for_list(hgp_ctx *c, const hgp_csr *g, uint32_t lo, const uint32_t *list, const uint32_t *list_count,
+                         uint32_t hcount, uint64_t *start, uint32_t *cnt, uint32_t **pool_out) {
+  hgp_status st = HGP_OK;
+  unsigned long long *misc = scratch_zero<unsigned long long>(c, 4, &st);   // sum, max, cursor, -
+  uint32_t *counters = scratch_zero<uint32_t>(c, 8, &st);
+  uint32_t *list1 = scratch_raw<uint32_t>(c, hcount ? hcount : 1, &st);
+  uint32_t *list2 = scratch_raw<uint32_t>(c, hcount ? hcount : 1, &st);
+  if (st) return st;
+  HGP_TRY(launch(c, "nbr_list_bound", k_list_bound_sum, dim3(c->sm_count), dim3(256), 0, (const uint64_t *)g->inc_off,
+                 (const uint32_t *)g->inc, (const uint64_t *)g->edge_off, list, list_count, g->N, misc, misc + 1));
+  uint64_t hb[2];
+  HGP_TRY(read_back(c, misc, 16, hb));
+  uint32_t *pool = scratch_raw<uint32_t>(c, hb[0] ? hb[0] : 1, &st);
+  if (st) return st;
+  *pool_out = pool;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_nbrs<kT1ThreadsL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT1LogL);
+    cudaFuncSetAttribute(k_nbrs<kT2ThreadsL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT2LogL);
+    attr = true;
+  }
+  NbrJob J{};
+  J.inc_off = g->inc_off; J.inc = g->inc; J.edge_off = g->edge_off; J.pins = g->pins;
+  J.lo = lo; J.pool = pool; J.pool_cap = hb[0] ? hb[0] : 1; J.pool_cursor = misc + 2;
+  J.start = start; J.cnt = cnt; J.pool_list = list2; J.pool_count = counters + 5;   // cannot overflow
+  J.list = list; J.list_count = list_count;
+  J.log2s = kT1LogL; J.cap = (1u << (kT1LogL - 1)) - 128 * (kT1ThreadsL / 32);
+  J.ovf_list = list1; J.ovf_count = counters + 0;
+  HGP_TRY(launch(c, "nbrs_list_t1", k_nbrs<kT1ThreadsL, true>, dim3(8u * c->sm_count), dim3(kT1ThreadsL), 4u << kT1LogL, J));
+  J.list = list1; J.list_count = counters + 0;
+  J.log2s = kT2LogL; J.cap = (1u << (kT2LogL - 1)) - 128 * (kT2ThreadsL / 32);
+  J.ovf_list = list2; J.ovf_count = counters + 1;
+  HGP_TRY(launch(c, "nbrs_list_t2", k_nbrs<kT2ThreadsL, true>, dim3(c->sm_count), dim3(kT2ThreadsL), 4u << kT2LogL, J));
+  if (hb[1] + 1 > (1u << (kT2LogL - 1)) - 128 * (kT2ThreadsL / 32)) {   // tier 3: global tables
+    uint32_t lg = 1;
+    while ((1ull << lg) < 2 * (hb[1] + 1) + 128 * 8) ++lg;
+    const uint32_t ctas = c->sm_count;
+    uint32_t *gtab = scratch_raw<uint32_t>(c, (size_t)ctas << lg, &st);
+    if (st) return st;
+    J.list = list2; J.list_count = counters + 1; J.log2s = lg; J.cap = 0xFFFFFFFFu; J.gtab = gtab;
+    J.ovf_list = list1; J.ovf_count = counters + 4;
+    HGP_TRY(launch(c, "nbrs_list_t3", k_nbrs<256, false>, dim3(ctas), dim3(256), 0, J));
+  }
+  return HGP_OK;
+}
+
 }  // namespace hgp
 
 using namespace hgp;

@@ -39,7 +39,9 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
   const uint32_t total = J.list_count ? *J.list_count : J.hi - J.lo;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = J.list ? J.list[t] : J.lo + t;
-    const uint64_t b0 = J.nb_off[n - J.lo], b1 = J.nb_off[n - J.lo + 1];
+    uint64_t b0, b1;
+    if (J.nb_off) { b0 = J.nb_off[n - J.lo]; b1 = J.nb_off[n - J.lo + 1]; }
+    else { b0 = J.nb_start[n - J.lo]; b1 = b0 + J.nb_len[n - J.lo]; }
     if (b1 - b0 > J.cap) {                                        // larger tier (CTA-uniform)
       if (tid == 0) J.big_list[atomicAdd(J.big_count, 1u)] = n;
       continue;
@@ -375,6 +377,16 @@ hgp_status score_run(hgp_ctx *c, const hgp_csr *g, hgp_nbrs *nb, const hgp_param
     else HGP_TRY(launch_score_tiers<16>(c, J, nn, nb->max_deg, lists, counts, list, list_count));
   }
   return score_finish(c);
+}
+
+hgp_status score_list_segments(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_deg, const uint32_t *list,
+                               const uint32_t *list_count) {
+  hgp_status st = HGP_OK;
+  uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
+  uint32_t *lists = scratch_raw<uint32_t>(c, 3 * (size_t)(nn ? nn : 1), &st);
+  if (st) return st;
+  if (J.pi <= 4) return launch_score_tiers<4>(c, J, nn, max_deg, lists, counts, list, list_count);
+  return launch_score_tiers<16>(c, J, nn, max_deg, lists, counts, list, list_count);
 }
 
 }  // namespace hgp

@@ -13,7 +13,9 @@ struct ScoreJob {
   const uint32_t *inc_nin, *inc, *in_mu;
   // neighbours
   uint32_t lo, hi;
-  const uint64_t *nb_off;
+  const uint64_t *nb_off;      // CSR offsets relative to lo, or nullptr: segments nb_start/nb_len
+  const uint64_t *nb_start;
+  const uint32_t *nb_len;
   uint32_t *nbr;
   // params
   uint64_t omega, delta, noise_cap, seed_mix;
@@ -145,5 +147,9 @@ hgp_status score_prologue(hgp_ctx *c, const hgp_csr *g, uint32_t lo, uint32_t hi
 hgp_status score_finish(hgp_ctx *c);
 hgp_status score_run(hgp_ctx *c, const hgp_csr *g, hgp_nbrs *nb, const hgp_params *p, hgp_cand *cand,
                      const uint32_t *list, const uint32_t *list_count);
+// a3 for the nodes of a device list whose neighbours are segments start/len of nbr (relative
+// to lo), with purge flags written in place; max_deg bounds the segment lengths.
+hgp_status score_list_segments(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_deg, const uint32_t *list,
+                               const uint32_t *list_count);
 
 }  // namespace hgp

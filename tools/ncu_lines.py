@@ -51,6 +51,8 @@ def main(rep, kregex, mangled, top=30):
     agg = {}
     tot_e = tot_s = 0
     for x in rows:
+        if len(x) <= max(ai, ei, si) or not x[ai].startswith("0x"):
+            break                                   # next kernel's section
         off = int(x[ai], 16) - base
         e = int(x[ei]) if x[ei].isdigit() else 0
         s = int(x[si]) if x[si].isdigit() else 0
