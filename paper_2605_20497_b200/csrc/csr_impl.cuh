@@ -16,7 +16,7 @@ struct SegView {
   uint64_t V;
 };
 hgp_status nbrs_for_list(hgp_ctx *c, const hgp_csr *g, uint32_t lo, const uint32_t *list, const uint32_t *list_count,
-                         uint32_t hcount, uint64_t *start, uint32_t *cnt, uint32_t **pool_out);
+                         uint32_t hcount, const uint32_t *base, uint64_t *start, uint32_t *cnt, uint32_t *max_deg_out);
 hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, uint32_t lo, uint32_t hi,
                             hgp_nbrs *out, hgp_cand *cand, SegView *view);
 hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match, uint32_t *gamma,

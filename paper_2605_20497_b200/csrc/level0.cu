@@ -9,7 +9,7 @@
 // traversals of the T = sum_e |e|(|e|-1) pin visits by one; results are identical to
 // hgp_unique_neighbors followed by hgp_score_pairs (same integer sums, same tie rules).
 // Nodes the packed form cannot represent, or whose neighbourhood overflows the largest shared
-// table, are handled by the unfused kernels (the whole call falls back if any node does).
+// table, are handled by the unfused kernels (list mode, over the same segment view).
 #include <cstdlib>
 
 #include "csr_impl.cuh"
@@ -30,7 +30,9 @@ struct FusedJob {
   unsigned long long *pool_cursor;
   uint64_t *start;                // [hi-lo] pool offset of each node's N(n)
   uint32_t *cnt;                  // [hi-lo]
-  uint32_t *defer_list, *defer_count;
+  uint32_t *defer_list, *defer_count;     // table too small / wide -> next tier
+  uint32_t *pool_list, *pool_count;       // pool full (cnt[n] holds the exact count) -> second pool
+  uint64_t start_bias;                    // added to every start written
 };
 
 // Phase 2b + 3 of k_nbrscore. PACKED: every score of the node is < 2^32, so (score, id) is
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
   uint32_t *acc = keys + S;
   uint16_t *ulist = reinterpret_cast<uint16_t *>(acc + S);        // dense list of neighbour slots (S <= 65536)
   const uint32_t keys_s = opaque_u32(smem_u32addr(keys)), acc_s = opaque_u32(smem_u32addr(acc));
-  const uint32_t hmask = S - 1, hshift = 32u - log2s;
+  const uint32_t hmask = S - 1;
   const uint32_t total = F.list_count ? *F.list_count : J.hi - J.lo;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = F.list ? F.list[t] : J.lo + t;
@@ -256,7 +258,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       } else {
         const unsigned long long st = atomicAdd(F.pool_cursor, (unsigned long long)acc0);
         s_start = st;
-        if (st + acc0 > F.pool_cap) { s_defer = 1; F.defer_list[atomicAdd(F.defer_count, 1u)] = n; }
+        if (st + acc0 > F.pool_cap) {
+          s_defer = 1;
+          F.cnt[n - J.lo] = acc0;
+          F.pool_list[atomicAdd(F.pool_count, 1u)] = n;
+        }
       }
     }
     __syncthreads();
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
     const uint32_t count = s_count;
     // ---- phase 2b: validity (Eq.6), flags, the N(n) entries with their flags,
     // noise, per-thread top-pi; phase 3: top-pi merge (warps, then warp 0)
-    if (tid == 0) F.start[n - J.lo] = s_start;
+    if (tid == 0) F.start[n - J.lo] = s_start + F.start_bias;
     if (tid == 0) F.cnt[n - J.lo] = count;
     if (s_small) eval_top<PIMAX, THREADS, true>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
     else eval_top<PIMAX, THREADS, false>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
@@ -306,37 +312,74 @@ __global__ void k_pairs_total(const uint64_t *edge_off, uint32_t E, unsigned lon
   if (lane_id() == 0) atomicAdd(T, (unsigned long long)s);
 }
 
-// tiers of the fused kernel: 4096 slots (40 KB incl. list, 128 threads) for every node, then
-// 16384 slots (160 KB, 256 threads) for the ones that overflowed
-static constexpr uint32_t kFALog = 12, kFAThreads = 128;
-static constexpr uint32_t kFBLog = 14, kFBThreads = 256;
+// tiers of the fused kernel: A 4096 slots (40 KB incl. the dense list) for every node, M 8192
+// slots (72 KB, 3 CTAs/SM), B 16384 slots (144 KB, 1 CTA/SM); what B cannot hold (or the packed
+// accumulator cannot represent) goes to the unfused kernels.
+static constexpr uint32_t kFALog = 12, kFMLog = 13, kFBLog = 14;
+static constexpr uint32_t kFMThreads = 256, kFBThreads = 256;
+
+struct TierLists {
+  const uint32_t *in_list, *in_count;   // nullptr: every node of [lo, hi)
+  uint32_t hn;                          // host upper bound of the input count (grid sizing)
+  uint32_t *la, *ca, *lm, *cm;          // A -> M, M -> B hand-off
+  uint32_t *ld, *cd;                    // B -> unfused (appended)
+};
+
+constexpr uint32_t fused_smem(uint32_t lg) { return (8u << lg) + (2u << (lg - 1)); }
 
 template <int PIMAX, int TA, int MINB>
-hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, uint32_t nn, uint32_t *lists, uint32_t *counts) {
+hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
   static bool attr = false;
-  constexpr uint32_t smemA = (8u << kFALog) + (2u << (kFALog - 1)), smemB = (8u << kFBLog) + (2u << (kFBLog - 1));
   if (!attr) {
-    cudaFuncSetAttribute(k_nbrscore<TA, PIMAX, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemA);
-    cudaFuncSetAttribute(k_nbrscore<kFBThreads, PIMAX, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemB);
+    cudaFuncSetAttribute(k_nbrscore<TA, PIMAX, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused_smem(kFALog));
+    cudaFuncSetAttribute(k_nbrscore<kFMThreads, PIMAX, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         fused_smem(kFMLog));
+    cudaFuncSetAttribute(k_nbrscore<kFBThreads, PIMAX, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         fused_smem(kFBLog));
     attr = true;
   }
-  F.list = nullptr; F.list_count = nullptr; F.log2s = kFALog;
-  F.defer_list = lists; F.defer_count = counts + 0;
+  const uint32_t sm = c->sm_count;
+  F.list = L.in_list; F.list_count = L.in_count; F.log2s = kFALog;
+  F.defer_list = L.la; F.defer_count = L.ca;
   const uint32_t per_sm = TA == 128 ? 32u : 16u;
-  const uint32_t gA = nn < per_sm * c->sm_count ? nn : per_sm * c->sm_count;
-  HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB>, dim3(gA), dim3(TA), smemA, F));
-  F.list = lists; F.list_count = counts + 0; F.log2s = kFBLog;
-  F.defer_list = lists + nn; F.defer_count = counts + 1;
-  HGP_TRY(launch(c, "nbrscore_B", k_nbrscore<kFBThreads, PIMAX, 1>, dim3(c->sm_count), dim3(kFBThreads), smemB, F));
+  const uint32_t gA = L.hn < per_sm * sm ? L.hn : per_sm * sm;
+  if (gA == 0) return HGP_OK;
+  HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
+  F.list = L.la; F.list_count = L.ca; F.log2s = kFMLog;
+  F.defer_list = L.lm; F.defer_count = L.cm;
+  HGP_TRY(launch(c, "nbrscore_M", k_nbrscore<kFMThreads, PIMAX, 3>, dim3(3 * sm), dim3(kFMThreads), fused_smem(kFMLog), F));
+  F.list = L.lm; F.list_count = L.cm; F.log2s = kFBLog;
+  F.defer_list = L.ld; F.defer_count = L.cd;
+  HGP_TRY(launch(c, "nbrscore_B", k_nbrscore<kFBThreads, PIMAX, 1>, dim3(sm), dim3(kFBThreads), fused_smem(kFBLog), F));
   return HGP_OK;
 }
 
 template <int PIMAX>
-hgp_status fused_tiers(hgp_ctx *c, FusedJob F, uint32_t nn, uint32_t *lists, uint32_t *counts) {
+hgp_status fused_tiers(hgp_ctx *c, FusedJob F, const TierLists &L) {
   static const int cfg = getenv("HGP_FUSED_CFG") ? atoi(getenv("HGP_FUSED_CFG")) : 1;
-  if (cfg == 1) return fused_tiers_t<PIMAX, 256, 6>(c, F, nn, lists, counts);
-  if (cfg == 2) return fused_tiers_t<PIMAX, 256, 4>(c, F, nn, lists, counts);
-  return fused_tiers_t<PIMAX, 256, 5>(c, F, nn, lists, counts);
+  if (cfg == 1) return fused_tiers_t<PIMAX, 256, 6>(c, F, L);
+  if (cfg == 2) return fused_tiers_t<PIMAX, 256, 4>(c, F, L);
+  return fused_tiers_t<PIMAX, 256, 5>(c, F, L);
+}
+
+__global__ void k_list_cnt_sum(const uint32_t *list, const uint32_t *count, const uint32_t *cnt, uint32_t lo,
+                               unsigned long long *sum) {
+  uint64_t s = 0;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < *count; t += gridDim.x * blockDim.x) s += cnt[list[t] - lo];
+  s = warp_sum(s);
+  if (lane_id() == 0 && s) atomicAdd(sum, (unsigned long long)s);
+}
+
+__global__ void k_iota(uint32_t *list, uint32_t *count, uint32_t lo, uint32_t nn) {
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += gridDim.x * blockDim.x) list[t] = lo + t;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = nn;
+}
+
+__global__ void k_cnt_sum(const uint32_t *cnt, uint32_t nn, unsigned long long *sum) {
+  uint64_t s = 0;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += gridDim.x * blockDim.x) s += cnt[t];
+  s = warp_sum(s);
+  if (lane_id() == 0 && s) atomicAdd(sum, (unsigned long long)s);
 }
 
 // a2 + a3 on a level-0 CSR (no flags yet). Returns the same nb and cand as hgp_unique_neighbors
@@ -349,35 +392,71 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   HGP_TRY(score_prologue(c, g, lo, hi, p, &J));
   J.cand = cand;
   hgp_status st = HGP_OK;
-  unsigned long long *misc = scratch_zero<unsigned long long>(c, 2, &st);    // T, pool cursor
-  uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
+  unsigned long long *misc = scratch_zero<unsigned long long>(c, 4, &st);    // T, cursor, cursor 2, sum
+  uint32_t *counts = scratch_zero<uint32_t>(c, 16, &st);
   uint64_t *start = scratch_raw<uint64_t>(c, nn, &st);
   uint32_t *cnt = scratch_raw<uint32_t>(c, nn, &st);
-  uint32_t *lists = scratch_raw<uint32_t>(c, 2 * (size_t)(nn ? nn : 1), &st);
+  uint32_t *lists = scratch_raw<uint32_t>(c, 4 * (size_t)(nn ? nn : 1), &st);
   if (st) return st;
   if (nn == 0) return HGP_E_INTERNAL;   // handled by the caller's fallback
   HGP_TRY(launch(c, "pairs_total", k_pairs_total, dim3(g->E ? (div_up(g->E, 256) < 1024 ? div_up(g->E, 256) : 1024) : 0),
                  dim3(256), 0, (const uint64_t *)g->edge_off, g->E, misc));
   uint64_t T = 0;
   HGP_TRY(read_u64(c, (const uint64_t *)misc, &T));
-  // pool estimate: min(T, 24 P) scaled to the range (nodes that do not fit make the call fall back)
+  // pool estimate: min(T, 24 P) scaled to the range; nodes that do not fit get a second, exact pool
   const double frac = g->N ? (double)nn / g->N : 1.0;
   uint64_t pool_cap = (uint64_t)((T < 24 * g->P ? T : 24 * g->P) * (frac < 1.0 ? 1.25 * frac : 1.0)) + nn;
+  // test hooks (tests/test_gpu_parity.py): a tiny first pool, or every node on the unfused path
+  const char *tp = getenv("HGP_TEST_FUSED_POOL");
+  if (tp) pool_cap = strtoull(tp, nullptr, 10);
+  const bool all_unfused = getenv("HGP_TEST_UNFUSED") != nullptr;
   if (pool_cap == 0) pool_cap = 1;
   uint32_t *pool = scratch_raw<uint32_t>(c, pool_cap, &st);
   if (st) return st;
+  uint32_t *LA = lists, *LM = lists + nn, *LD = lists + 2 * (size_t)nn, *LP = lists + 3 * (size_t)nn;
+  // counts: 0 A->M, 1 M->B, 2 deferred (unfused), 3 pool overflow, 4/5 second pass A->M / M->B,
+  // 6 second-pass pool overflow (impossible: exact pool), 7 max degree
   FusedJob F{};
   F.S = J;
   F.pool = pool; F.pool_cap = pool_cap; F.pool_cursor = misc + 1; F.start = start; F.cnt = cnt;
-  if (p->pi <= 4) HGP_TRY(fused_tiers<4>(c, F, nn, lists, counts));
-  else HGP_TRY(fused_tiers<16>(c, F, nn, lists, counts));
-  uint32_t hc[2];
-  HGP_TRY(read_back(c, counts, 8, hc));
-  if (hc[1]) return HGP_E_INTERNAL;      // some node needs the unfused path: caller falls back
+  F.pool_list = LP; F.pool_count = counts + 3;
+  TierLists L{nullptr, nullptr, nn, LA, counts + 0, LM, counts + 1, LD, counts + 2};
+  if (all_unfused) HGP_TRY(launch(c, "iota", k_iota, dim3(div_up(nn, 256) < 4096 ? div_up(nn, 256) : 4096), dim3(256), 0,
+                                  LD, counts + 2, lo, nn));
+  else if (p->pi <= 4) HGP_TRY(fused_tiers<4>(c, F, L));
+  else HGP_TRY(fused_tiers<16>(c, F, L));
+  uint32_t hc[8];
+  HGP_TRY(read_back(c, counts, sizeof(hc), hc));
+  if (hc[3]) {   // second pool, exactly the recorded counts of the pool-overflow nodes
+    HGP_TRY(launch(c, "list_cnt_sum", k_list_cnt_sum, dim3(c->sm_count), dim3(256), 0, (const uint32_t *)LP,
+                   (const uint32_t *)(counts + 3), (const uint32_t *)cnt, lo, misc + 3));
+    uint64_t need = 0;
+    HGP_TRY(read_u64(c, (const uint64_t *)(misc + 3), &need));
+    uint32_t *pool2 = scratch_raw<uint32_t>(c, need ? need : 1, &st);
+    if (st) return st;
+    FusedJob F2 = F;
+    F2.pool = pool2; F2.pool_cap = need ? need : 1; F2.pool_cursor = misc + 2;
+    F2.start_bias = (uint64_t)(pool2 - pool);
+    F2.pool_list = LA; F2.pool_count = counts + 6;
+    TierLists L2{LP, counts + 3, hc[3], LA, counts + 4, LM, counts + 5, LD, counts + 2};
+    if (p->pi <= 4) HGP_TRY(fused_tiers<4>(c, F2, L2));
+    else HGP_TRY(fused_tiers<16>(c, F2, L2));
+    HGP_TRY(read_back(c, counts, sizeof(hc), hc));
+    if (hc[6]) return set_error(HGP_E_INTERNAL, "fused a2+a3: exact second pool overflowed");
+  }
+  if (hc[2]) {   // unfused a2 + a3 for the nodes no fused tier could take (same results)
+    uint32_t md = 0;
+    HGP_TRY(nbrs_for_list(c, g, lo, LD, counts + 2, hc[2], pool, start, cnt, &md));
+    ScoreJob J3 = J;
+    J3.nb_off = nullptr; J3.nb_start = start; J3.nb_len = cnt; J3.nbr = pool;
+    HGP_TRY(score_list_segments(c, J3, hc[2], md, LD, counts + 2));
+  }
   HGP_TRY(score_finish(c));
   if (!out) {   // leave N(n) in the pool: segment n = pool[start[n] .. + cnt[n]) (relative to lo)
+    HGP_CUDA(cudaMemsetAsync(misc + 3, 0, 8, c->stream));
+    HGP_TRY(launch(c, "cnt_sum", k_cnt_sum, dim3(c->sm_count), dim3(256), 0, (const uint32_t *)cnt, nn, misc + 3));
     uint64_t V = 0;
-    HGP_TRY(read_u64(c, (const uint64_t *)(misc + 1), &V));
+    HGP_TRY(read_u64(c, (const uint64_t *)(misc + 3), &V));
     view->start = start; view->len = cnt; view->nbr = pool; view->V = V;
     return HGP_OK;
   }
@@ -390,7 +469,7 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   out->V = V;
   out->nbr = dalloc_n<uint32_t>(c, V, &st);
   if (st) return st;
-  unsigned int *d_max = counts + 2;
+  unsigned int *d_max = counts + 7;
   HGP_TRY(launch(c, "fused_pack", k_fused_pack, dim3(nn / 8 + 1 < 16u * c->sm_count ? nn / 8 + 1 : 16u * c->sm_count),
                  dim3(256), 0, (const uint32_t *)pool, (const uint64_t *)start, (const uint32_t *)cnt,
                  (const uint64_t *)out->off, nn, out->nbr, d_max));

@@ -29,6 +29,7 @@ struct NbrJob {
   uint32_t *cnt;               // [hi-lo]
   uint32_t *ovf_list, *ovf_count;    // table overflow -> next tier
   uint32_t *pool_list, *pool_count;  // pool overflow -> rerun after growing the pool
+  uint64_t start_bias;               // added to every start written (pool base differs from the view's)
 };
 
 template <int THREADS, bool SMEM>
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
     const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1];
     volatile uint32_t *vcnt = &s_cnt;
     const uint32_t tab_s = SMEM ? opaque_u32(smem_u32addr(tab)) : 0u;
-    const uint32_t hmask = S - 1, hshift = 32u - J.log2s;
+    const uint32_t hmask = S - 1;
     bool stop = false;
     uint32_t nins = 0;                                             // new keys, flushed per block
     // a warp loads the offsets of 32 incident edges at once (lane = edge), then walks them with
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
         wpos = __shfl_sync(0xFFFFFFFFu, wpos, 0);
         if (has) J.pool[s_start + wpos + __popc(bal & lt)] = v;
       }
-      if (tid == 0) { J.start[n - J.lo] = s_start; J.cnt[n - J.lo] = count; }
+      if (tid == 0) { J.start[n - J.lo] = s_start + J.start_bias; J.cnt[n - J.lo] = count; }
     }
     __syncthreads();
   }
@@ -222,53 +223,72 @@ __global__ void k_list_bound_sum(const uint64_t *inc_off, const uint32_t *inc, c
 static constexpr uint32_t kT1LogL = 12, kT1ThreadsL = 128;
 static constexpr uint32_t kT2LogL = 15, kT2ThreadsL = 256;
 
-// a2 for the nodes of a device list (hcount = its host-known length): N(n) into a pool sized by
-// the exact bound sum_n min(sum_{e in I(n)} (|e|-1), N-1), so nothing can overflow.
-// start/cnt are indexed n - lo; *pool_out is scratch of the current call.
+// a2 for the nodes of a device list (hcount = its host-known length): N(n) into a fresh pool
+// sized min(exact bound, 8 P + hcount), with bound = sum_n min(sum_{e in I(n)} (|e|-1), N-1); a
+// too-short pool is regrown once to the exact total (the cursor). start/cnt are indexed n - lo,
+// start relative to `base`; *max_deg_out = an upper bound of the counts.
 hgp_status nbrs_for_list(hgp_ctx *c, const hgp_csr *g, uint32_t lo, const uint32_t *list, const uint32_t *list_count,
-                         uint32_t hcount, uint64_t *start, uint32_t *cnt, uint32_t **pool_out) {
+                         uint32_t hcount, const uint32_t *base, uint64_t *start, uint32_t *cnt, uint32_t *max_deg_out) {
   hgp_status st = HGP_OK;
   unsigned long long *misc = scratch_zero<unsigned long long>(c, 4, &st);   // sum, max, cursor, -
   uint32_t *counters = scratch_zero<uint32_t>(c, 8, &st);
   uint32_t *list1 = scratch_raw<uint32_t>(c, hcount ? hcount : 1, &st);
   uint32_t *list2 = scratch_raw<uint32_t>(c, hcount ? hcount : 1, &st);
+  uint32_t *plist = scratch_raw<uint32_t>(c, hcount ? hcount : 1, &st);
   if (st) return st;
   HGP_TRY(launch(c, "nbr_list_bound", k_list_bound_sum, dim3(c->sm_count), dim3(256), 0, (const uint64_t *)g->inc_off,
                  (const uint32_t *)g->inc, (const uint64_t *)g->edge_off, list, list_count, g->N, misc, misc + 1));
   uint64_t hb[2];
   HGP_TRY(read_back(c, misc, 16, hb));
-  uint32_t *pool = scratch_raw<uint32_t>(c, hb[0] ? hb[0] : 1, &st);
-  if (st) return st;
-  *pool_out = pool;
+  *max_deg_out = (uint32_t)hb[1];
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_nbrs<kT1ThreadsL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT1LogL);
     cudaFuncSetAttribute(k_nbrs<kT2ThreadsL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT2LogL);
     attr = true;
   }
-  NbrJob J{};
-  J.inc_off = g->inc_off; J.inc = g->inc; J.edge_off = g->edge_off; J.pins = g->pins;
-  J.lo = lo; J.pool = pool; J.pool_cap = hb[0] ? hb[0] : 1; J.pool_cursor = misc + 2;
-  J.start = start; J.cnt = cnt; J.pool_list = list2; J.pool_count = counters + 5;   // cannot overflow
-  J.list = list; J.list_count = list_count;
-  J.log2s = kT1LogL; J.cap = (1u << (kT1LogL - 1)) - 128 * (kT1ThreadsL / 32);
-  J.ovf_list = list1; J.ovf_count = counters + 0;
-  HGP_TRY(launch(c, "nbrs_list_t1", k_nbrs<kT1ThreadsL, true>, dim3(8u * c->sm_count), dim3(kT1ThreadsL), 4u << kT1LogL, J));
-  J.list = list1; J.list_count = counters + 0;
-  J.log2s = kT2LogL; J.cap = (1u << (kT2LogL - 1)) - 128 * (kT2ThreadsL / 32);
-  J.ovf_list = list2; J.ovf_count = counters + 1;
-  HGP_TRY(launch(c, "nbrs_list_t2", k_nbrs<kT2ThreadsL, true>, dim3(c->sm_count), dim3(kT2ThreadsL), 4u << kT2LogL, J));
-  if (hb[1] + 1 > (1u << (kT2LogL - 1)) - 128 * (kT2ThreadsL / 32)) {   // tier 3: global tables
-    uint32_t lg = 1;
+  uint32_t *gtab = nullptr;
+  uint32_t lg = 1;
+  const bool t3 = hb[1] + 1 > (1u << (kT2LogL - 1)) - 128 * (kT2ThreadsL / 32);
+  if (t3) {   // tier 3: global tables
     while ((1ull << lg) < 2 * (hb[1] + 1) + 128 * 8) ++lg;
-    const uint32_t ctas = c->sm_count;
-    uint32_t *gtab = scratch_raw<uint32_t>(c, (size_t)ctas << lg, &st);
+    gtab = scratch_raw<uint32_t>(c, (size_t)c->sm_count << lg, &st);
     if (st) return st;
-    J.list = list2; J.list_count = counters + 1; J.log2s = lg; J.cap = 0xFFFFFFFFu; J.gtab = gtab;
-    J.ovf_list = list1; J.ovf_count = counters + 4;
-    HGP_TRY(launch(c, "nbrs_list_t3", k_nbrs<256, false>, dim3(ctas), dim3(256), 0, J));
   }
-  return HGP_OK;
+  uint64_t pool_cap = hb[0] < 8 * g->P + hcount ? hb[0] : 8 * g->P + hcount;
+  for (int attempt = 0;; ++attempt) {
+    if (pool_cap == 0) pool_cap = 1;
+    uint32_t *pool = scratch_raw<uint32_t>(c, pool_cap, &st);
+    if (st) return st;
+    HGP_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(uint32_t), c->stream));
+    HGP_CUDA(cudaMemsetAsync(misc + 2, 0, sizeof(unsigned long long), c->stream));
+    NbrJob J{};
+    J.inc_off = g->inc_off; J.inc = g->inc; J.edge_off = g->edge_off; J.pins = g->pins;
+    J.lo = lo; J.pool = pool; J.pool_cap = pool_cap; J.pool_cursor = misc + 2;
+    J.start_bias = (uint64_t)(pool - base);
+    J.start = start; J.cnt = cnt; J.pool_list = plist; J.pool_count = counters + 5;
+    J.list = list; J.list_count = list_count;
+    J.log2s = kT1LogL; J.cap = (1u << (kT1LogL - 1)) - 128 * (kT1ThreadsL / 32);
+    J.ovf_list = list1; J.ovf_count = counters + 0;
+    HGP_TRY(launch(c, "nbrs_list_t1", k_nbrs<kT1ThreadsL, true>, dim3(8u * c->sm_count), dim3(kT1ThreadsL),
+                   4u << kT1LogL, J));
+    J.list = list1; J.list_count = counters + 0;
+    J.log2s = kT2LogL; J.cap = (1u << (kT2LogL - 1)) - 128 * (kT2ThreadsL / 32);
+    J.ovf_list = list2; J.ovf_count = counters + 1;
+    HGP_TRY(launch(c, "nbrs_list_t2", k_nbrs<kT2ThreadsL, true>, dim3(c->sm_count), dim3(kT2ThreadsL), 4u << kT2LogL, J));
+    if (t3) {
+      J.list = list2; J.list_count = counters + 1; J.log2s = lg; J.cap = 0xFFFFFFFFu; J.gtab = gtab;
+      J.ovf_list = list1; J.ovf_count = counters + 4;   // cannot overflow: table >= 2 (bound + 1)
+      HGP_TRY(launch(c, "nbrs_list_t3", k_nbrs<256, false>, dim3(c->sm_count), dim3(256), 0, J));
+    }
+    uint32_t hc[8];
+    HGP_TRY(read_back(c, counters, sizeof(hc), hc));
+    if (hc[5] == 0) return HGP_OK;
+    if (attempt == 1) return set_error(HGP_E_INTERNAL, "nbrs_for_list: pool sizing failed");
+    uint64_t cur = 0;
+    HGP_TRY(read_u64(c, (const uint64_t *)(misc + 2), &cur));
+    pool_cap = cur;
+  }
 }
 
 }  // namespace hgp

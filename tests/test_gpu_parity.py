@@ -278,3 +278,40 @@ def test_fused_level0_matches_oracle(hgp, ctx, name, make, omega, delta):
     assert np.array_equal(m2.cpu().numpy(), rr["match"]) and np.array_equal(gam2.cpu().numpy(), rr["gamma"])
     assert_csr_equal(cg2.to_host(), rr["coarse"], "fused coarse (pool view)")
     assert_nbrs_equal(cnb2.to_host(), rr["coarse_nb"], "fused coarse nbrs (pool view)")
+
+
+@pytest.mark.parametrize("mode", ["pool64", "pool1", "unfused"])
+@pytest.mark.parametrize("name,make,omega,delta", FUSED_CASES[1:], ids=[c[0] for c in FUSED_CASES[1:]])
+def test_fused_level0_partial_paths(hgp, ctx, monkeypatch, mode, name, make, omega, delta):
+    """The fused call's secondary paths give the same level: a first pool too small for most nodes
+    (second, exact pool), and every node on the unfused list path (k_nbrs + k_score over the
+    segment view) — both with and without returning N(n)."""
+    if mode.startswith("pool"):
+        monkeypatch.setenv("HGP_TEST_FUSED_POOL", mode[4:])
+    else:
+        monkeypatch.setenv("HGP_TEST_UNFUSED", "1")
+    hg = make()
+    cap = hgpgen.default_noise_cap(hg)
+    g = gpu_build(hgp, ctx, hg)
+    rg = ref.build_csr_hg(hg)
+    rnb = ref.unique_neighbors(rg)
+    rr = ref.coarsen_level(rg, rnb, ref.params(omega, delta, 4, noise_seed=2, noise_cap=cap))
+    for want in (True, False):
+        m = torch.empty(g.N, dtype=torch.uint32, device="cuda")
+        gam = torch.empty(g.N, dtype=torch.uint32, device="cuda")
+        cand = hgp.empty_cand(g.N, 4)
+        ctx.profile_begin("nbr")
+        nb, cg, cnb, st = hgp.coarsen_level0(ctx, g, hgp.params(omega, delta, 4, noise_seed=2, noise_cap=cap), cand,
+                                             m, gam, want_nbrs=want)
+        ctx.profile_end()
+        used = ctx.profile_report()
+        if mode == "unfused":
+            assert "nbrscore_A" not in used and "nbrs_list_t1" in used, used
+        if want:
+            assert_nbrs_equal(nb.to_host(), rnb, f"{mode} nbrs+flags")
+        assert st["V"] == rnb.nbr.shape[0]
+        assert_cand_equal(hgp.cand_to_numpy(cand), rr["cand"])
+        assert np.array_equal(m.cpu().numpy(), rr["match"])
+        assert np.array_equal(gam.cpu().numpy(), rr["gamma"])
+        assert_csr_equal(cg.to_host(), rr["coarse"], f"{mode} coarse")
+        assert_nbrs_equal(cnb.to_host(), rr["coarse_nb"], f"{mode} coarse nbrs")
