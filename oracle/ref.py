@@ -240,3 +240,35 @@ def coarsen_level(g: Csr, nb: Nbrs, p: CParams):
     gamma, cg, cnb = contract(g, nb, m)
     return {"cand": cand, "match": m, "matched_per_round": per, "round_value": val,
             "gamma": gamma, "coarse": cg, "coarse_nb": cnb}
+
+
+def stop_nodes(g0: Csr, omega: int) -> int:
+    """Reading #20 (coarsen until |N| reaches ceil(W/Omega) or no valid cluster is
+    left): the node count at or below which the multi-level driver stops; W = total size."""
+    W = int(g0.node_w.astype(np.uint64).sum())
+    return 1 if omega == UNBOUNDED else max(1, -(-W // int(omega)))
+
+
+def coarsen(g0: Csr, p: CParams, max_levels: int = 64) -> dict:
+    """Multi-level driver, written out plainly: level l is
+    coarsen_level on the previous level's coarse CSR and neighbour lists, with noise seed
+    p.noise_seed + l (reading #3: "the driver passes seed+level"); it stops after the first level
+    whose coarse node count is <= stop_nodes(g0, Omega) or that matched no pair (reading #20), or
+    after max_levels levels. rho = gamma^L o ... o gamma^1 maps each level-0 node to its node on
+    the coarsest level (the initial partition's clusters)."""
+    g, nb = g0, unique_neighbors(g0)
+    rho = np.arange(g0.N, dtype=np.uint32)
+    stop = stop_nodes(g0, p.omega)
+    levels = []
+    for lvl in range(max_levels):
+        pl = params(p.omega, p.delta, p.pi, norm=p.norm, noise_seed=p.noise_seed + lvl, noise_cap=p.noise_cap)
+        r = coarsen_level(g, nb, pl)
+        rho = r["gamma"][rho]
+        per = [int(x) for x in r["matched_per_round"]]
+        cg = r["coarse"]
+        levels.append({"N": g.N, "E": g.E, "P": g.P, "Nc": cg.N, "Ec": cg.E, "Pc": cg.P,
+                       "matched_per_round": per, "gamma": r["gamma"], "match": r["match"]})
+        g, nb = cg, r["coarse_nb"]
+        if g.N <= stop or sum(per) == 0:
+            break
+    return {"rho": rho, "levels": levels, "coarsest": g, "coarsest_nb": nb, "stop_nodes": stop}
