@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -105,6 +106,12 @@ inline hgp_status launch(hgp_ctx *c, const char *name, K kernel, dim3 grid, dim3
   kernel<<<grid, block, smem, c->stream>>>(args...);
   if (prof) { cudaEventRecord(e1, c->stream); c->prof_events.push_back({e0, e1}); c->prof_names.push_back(name); }
   c->launches++;
+  static const bool dbg = getenv("HGP_DEBUG_SYNC") != nullptr;   // debugging: serialise + trace
+  if (dbg) {
+    fprintf(stderr, "[hgp] %s grid %u block %u smem %zu ...", name, grid.x, block.x, smem);
+    cudaError_t se = cudaStreamSynchronize(c->stream);
+    fprintf(stderr, " %s\n", cudaGetErrorString(se));
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(HGP_E_CUDA, "launch %s: %s", name, cudaGetErrorString(e));
   return HGP_OK;
@@ -175,6 +182,17 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
 }
 __device__ __forceinline__ void red_add_u32(uint32_t a, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// predicated forms (no branch around the access)
+__device__ __forceinline__ void red_add_u32_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q red.shared.add.u32 [%0], %1;\n}" ::"r"(a), "r"(v),
+               "r"((uint32_t)p)
+               : "memory");
+}
+__device__ __forceinline__ void sts_u32_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.shared.u32 [%0], %1;\n}" ::"r"(a), "r"(v),
+               "r"((uint32_t)p)
+               : "memory");
 }
 __device__ __forceinline__ uint32_t cas_u32(uint32_t a, uint32_t cmp, uint32_t val) {
   uint32_t old;

@@ -33,6 +33,7 @@ struct FusedJob {
   uint32_t *defer_list, *defer_count;     // table too small / wide -> next tier
   uint32_t *pool_list, *pool_count;       // pool full (cnt[n] holds the exact count) -> second pool
   uint64_t start_bias;                    // added to every start written
+  const uint64_t *cv;                     // [E] c(e), Eq.5 term in 2^-24 fixed point
 };
 
 // Phase 2b + 3 of k_nbrscore. PACKED: every score of the node is < 2^32, so (score, id) is
@@ -108,50 +109,80 @@ __device__ __forceinline__ void eval_top(const ScoreJob &J, const FusedJob &F, u
   }
 }
 
-template <int THREADS, int PIMAX, int MINB>
+// Shared-memory layout of k_nbrscore: keys[S] | acc[S] | dense slot list u16[S/2] | edge rows
+// of the current tile (A: {pointer to pins[edge start] - flat start, flat start of dst(e), add of a
+// src pin}, B: {flat end, add of a dst pin}).
+constexpr uint32_t kKT = 128;     // incident edges per tile
+constexpr uint32_t fused_smem(uint32_t lg) { return (9u << lg) + kKT * 24u; }
+
+// predicated shared CAS: lanes with p == false return `dflt` without touching memory
+__device__ __forceinline__ uint32_t cas_u32_if(bool p, uint32_t a, uint32_t cmp, uint32_t val, uint32_t dflt) {
+  uint32_t old = dflt;
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %4, 0;\n @q atom.shared.cas.b32 %0, [%1], %2, %3;\n}"
+               : "+r"(old)
+               : "r"(a), "r"(cmp), "r"(val), "r"((uint32_t)p)
+               : "memory");
+  return old;
+}
+
+// One CTA per node n (grid-stride over the node list): the fused a2 + a3 traversal of I(n).
+//  phase 0  sum and gcd of c(e) over I(n): is the packed 32-bit accumulator exact?
+//  phase 1  per tile of kKT incident edges: edge rows in shared memory (block scan of |e|), then
+//           the tile's pins are one flat sequence split evenly over the warps (no idle lanes
+//           whatever |e|; each lane tracks its current edge). Per pin, straight-line and
+//           predicated: one shared load of the home slot; an empty home slot is claimed with one
+//           shared CAS (first visit); if the home slot then holds the key, the packed term is
+//           added with one native shared atomic. Only keys displaced by a collision (a fraction
+//           of a percent at load <= 1/4 with the multiplicative hash) take the divergent
+//           linear-probing path, entered by the warp only when some lane needs it.
+//  phase 2  dense list of the occupied slots (one sweep, block scan), then validity, purge
+//           flags, noise and top-Pi over it; N(n) to the pool.
+//  reset    only the slots used (the table is cleared once per CTA).
+template <int THREADS, int PIMAX, int MINB, int LOG2S>
 __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
   extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ uint64_t s_tops[(THREADS / 32 + 1) * PIMAX];
-  __shared__ uint32_t s_topi[(THREADS / 32 + 1) * PIMAX];
-  __shared__ uint64_t s_sum[THREADS / 32], s_g[THREADS / 32];
-  __shared__ uint32_t s_defer, s_ib, s_count, s_small;
-  __shared__ uint32_t s_wcnt[THREADS / 32];
+  constexpr uint32_t NW = THREADS / 32;
+  static_assert(THREADS >= (int)kKT, "one edge row per thread");
+  __shared__ uint64_t s_tops[(NW + 1) * PIMAX];
+  __shared__ uint32_t s_topi[(NW + 1) * PIMAX];
+  __shared__ uint64_t s_sum[NW], s_g[NW];
+  __shared__ uint32_t s_wsum[NW];
+  __shared__ uint32_t s_defer, s_ib, s_small, s_full, s_self;
   __shared__ uint64_t s_gcd;
   __shared__ unsigned long long s_start;
-  constexpr uint32_t NW = THREADS / 32;
   const ScoreJob &J = F.S;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint32_t log2s = F.log2s, S = 1u << log2s;
+  constexpr uint32_t log2s = LOG2S, S = 1u << LOG2S, ucap = S / 2, hmask = S - 1;
   uint32_t *keys = reinterpret_cast<uint32_t *>(dyn);
   uint32_t *acc = keys + S;
-  uint16_t *ulist = reinterpret_cast<uint16_t *>(acc + S);        // dense list of neighbour slots (S <= 65536)
-  const uint32_t keys_s = opaque_u32(smem_u32addr(keys)), acc_s = opaque_u32(smem_u32addr(acc));
-  const uint32_t hmask = S - 1;
+  uint16_t *ulist = reinterpret_cast<uint16_t *>(acc + S);
+  uint4 *rowA = reinterpret_cast<uint4 *>(ulist + S / 2);
+  uint2 *rowB = reinterpret_cast<uint2 *>(rowA + kKT);
+  const uint32_t keys_s = smem_u32addr(keys), acc_s = smem_u32addr(acc);
   const uint32_t total = F.list_count ? *F.list_count : J.hi - J.lo;
+  for (uint32_t i = tid; i < S / 4; i += THREADS) {
+    reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    reinterpret_cast<uint4 *>(acc)[i] = make_uint4(0, 0, 0, 0);
+  }
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = F.list ? F.list[t] : J.lo + t;
     const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1], iin = i0 + J.inc_nin[n];
     const uint32_t inn = J.in_mu[n];
-    // ---- phase 0: gcd / sum of c(e) over I(n): is the packed 32-bit accumulator exact?
+    // ---- phase 0
     uint64_t sum = 0, gg = 0;
     for (uint64_t k = i0 + tid; k < i1; k += THREADS) {
-      const uint32_t e = J.inc[k];
-      const uint64_t a = J.edge_off[e], b = J.edge_off[e + 1];
-      const uint64_t ce = edge_c(J, e, a, b);
+      const uint64_t ce = F.cv[J.inc[k]];
       sum += ce;
       gg = gcd64(gg, ce);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-      gg = gcd64(gg, __shfl_xor_sync(0xFFFFFFFFu, gg, o));
+      const uint64_t og = __shfl_xor_sync(0xFFFFFFFFu, gg, o);
+      if (og != gg) gg = gcd64(gg, og);
     }
     if (lane == 0) { s_sum[w] = sum; s_g[w] = gg; }
-    for (uint32_t i = tid; i < S / 4; i += THREADS) {
-      reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-      reinterpret_cast<uint4 *>(acc)[i] = make_uint4(0, 0, 0, 0);
-    }
-    __syncthreads();
+    __syncthreads();   // also: the table is clean (initial clear / previous node's reset)
     if (tid == 0) {
       uint64_t S1 = 0, G1 = 0;
       for (uint32_t q = 0; q < NW; ++q) { S1 += s_sum[q]; G1 = gcd64(G1, s_g[q]); }
@@ -162,7 +193,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       s_gcd = G1;
       s_ib = bits;
       s_small = (unsigned __int128)S1 + J.noise_cap < ((unsigned __int128)1 << 32);
-      hs_insert(keys, log2s, n);                                 // self-visits land in n's slot
+      s_full = 0;
+      if (!s_defer) {
+        bool ins = false;
+        s_self = hs_insert_slot(keys, log2s, n, &ins);            // self-visits land in n's slot
+      }
     }
     __syncthreads();
     if (s_defer) {
@@ -172,118 +207,175 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
     }
     const uint64_t g = s_gcd;
     const uint32_t ib = s_ib;
-    // ---- phase 1 (= a2 + a3 traversal): insert-or-find every pin, add its packed term.
-    // No counter in the hot loop: a probe sequence longer than kProbeCap means the table is
-    // (nearly) full, and the node goes to the next tier (results of a deferred node are unused).
-    bool stop = false;
-    for (uint64_t kb = i0 + w; kb < i1 && !stop; kb += (uint64_t)NW * 32) {
-      const uint64_t k = kb + (uint64_t)NW * lane;
+    // ---- phase 1, tile by tile
+    for (uint64_t t0 = i0; t0 < i1; t0 += kKT) {
+      const uint32_t kt = (uint32_t)min((uint64_t)kKT, i1 - t0);
+      uint32_t len = 0, ns = 0, as = 0, ad = 0;
       uint64_t a = 0;
-      uint32_t len = 0, srel = 0, add_s = 0, add_d = 0;
-      if (k < i1) {
-        const uint32_t e = J.inc[k];
+      if (tid < kt) {
+        const uint32_t e = J.inc[t0 + tid];
         a = J.edge_off[e];
-        const uint64_t b = J.edge_off[e + 1];
-        len = (uint32_t)(b - a);
-        srel = J.edge_nsrc[e];
-        add_s = (uint32_t)((edge_c(J, e, a, b) / g) << ib);
-        add_d = add_s + (k < iin ? J.edge_mu[e] : 0u);             // m in dst(e), e in in(n)
+        len = (uint32_t)(J.edge_off[e + 1] - a);
+        ns = J.edge_nsrc[e];
+        const uint64_t ce = F.cv[e];
+        as = (uint32_t)((ce == g ? 1ull : ce / g) << ib);
+        ad = as + (t0 + tid < iin ? J.edge_mu[e] : 0u);           // m in dst(e), e in in(n)
       }
-      const uint32_t cnt = (uint32_t)min((uint64_t)32, (i1 - kb + NW - 1) / NW);
-      for (uint32_t j = 0; j < cnt && !stop; ++j) {
-        const uint64_t aj = __shfl_sync(0xFFFFFFFFu, a, j);
-        const uint32_t lj = __shfl_sync(0xFFFFFFFFu, len, j);
-        const uint32_t sj = __shfl_sync(0xFFFFFFFFu, srel, j);
-        const uint32_t as_j = __shfl_sync(0xFFFFFFFFu, add_s, j);
-        const uint32_t ad_j = __shfl_sync(0xFFFFFFFFu, add_d, j);
-        const uint32_t *pj = J.pins + aj;
-        for (uint32_t b4 = 0; b4 < lj; b4 += 128) {
-          uint32_t m[4], sl[4], kk[4];
+      const uint32_t incl = warp_incl_scan(len);
+      if (lane == 31) s_wsum[w] = incl;
+      __syncthreads();
+      uint32_t woff = 0, tot = 0;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t idx = b4 + u * 32 + lane;
-            m[u] = idx < lj ? __ldg(pj + idx) : kEmpty;
+      for (uint32_t q = 0; q < NW; ++q) { const uint32_t x = s_wsum[q]; woff += q < w ? x : 0u; tot += x; }
+      if (tid < kt) {
+        const uint32_t ex = woff + incl - len;
+        const uint64_t pp = reinterpret_cast<uint64_t>(J.pins + a) - 4ull * ex;   // &pins[a] - ex
+        rowA[tid] = make_uint4((uint32_t)pp, (uint32_t)(pp >> 32), ex + ns, as);
+        rowB[tid] = make_uint2(ex + len, ad);
+      }
+      __syncthreads();
+      // this warp's share of the tile's flat pin sequence
+      const uint32_t flo = (uint32_t)(((uint64_t)tot * w) / NW), fhi = (uint32_t)(((uint64_t)tot * (w + 1)) / NW);
+      uint32_t k = 0;
+      {
+        const uint32_t f = flo + lane;                             // first row whose end exceeds f
+        uint32_t lo_ = 0, hi_ = kt - 1;
+        while (lo_ < hi_) {
+          const uint32_t mid = (lo_ + hi_) >> 1;
+          if (rowB[mid].x > f) hi_ = mid; else lo_ = mid + 1;
+        }
+        k = lo_;
+      }
+      uint4 ra = rowA[k];
+      uint2 rb = rowB[k];
+      bool full = false;
+      for (uint32_t f0 = flo; f0 < fhi; f0 += 128) {
+        uint32_t m[4], add[4], sl[4], kk[4];
+        bool val[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t f = f0 + u * 32 + lane;
+          val[u] = f < fhi;
+          if (val[u]) {
+            while (f >= rb.x) { ++k; ra = rowA[k]; rb = rowB[k]; }   // next incident edge
           }
+          const uint32_t *pf = reinterpret_cast<const uint32_t *>(((uint64_t)ra.y << 32) | ra.x) + f;
+          m[u] = val[u] ? __ldg(pf) : 0u;
+          add[u] = f >= ra.z ? rb.y : ra.w;
+        }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) sl[u] = hash_slot(m[u], log2s);
+        for (int u = 0; u < 4; ++u) {
+          sl[u] = hash_slot(m[u], log2s);
+          kk[u] = lds_u32(keys_s + 4 * sl[u]);
+        }
+        uint32_t any_miss = 0;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) kk[u] = lds_u32(keys_s + 4 * sl[u]);
-          bool full = false;
+        for (int u = 0; u < 4; ++u) {
+          // valid: claim an empty home (CAS); hit if the home now holds m; add; else miss
+          uint32_t miss;
+          asm volatile(
+              "{\n .reg .pred pv, pc, ph;\n .reg .b32 o;\n"
+              " setp.ne.u32 pv, %2, 0;\n"
+              " setp.eq.and.u32 pc, %3, -1, pv;\n"
+              " mov.b32 o, %3;\n"
+              " @pc atom.shared.cas.b32 o, [%1], -1, %4;\n"
+              " setp.eq.u32 ph, o, %4;\n"
+              " setp.eq.or.u32 ph, o, -1, ph;\n"
+              " and.pred ph, ph, pv;\n"
+              " @ph red.shared.add.u32 [%1+%6], %5;\n"
+              " not.pred ph, ph;\n"
+              " and.pred ph, ph, pv;\n"
+              " selp.u32 %0, 1, 0, ph;\n}"
+              : "=r"(miss)
+              : "r"(keys_s + 4 * sl[u]), "r"((uint32_t)val[u]), "r"(kk[u]), "r"(m[u]), "r"(add[u]), "n"(4 * S)
+              : "memory");
+          val[u] = miss != 0;                                      // val now marks the misses
+          any_miss |= miss;
+        }
+        if (__any_sync(0xFFFFFFFFu, any_miss != 0)) {                   // displaced keys: probe on
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            if (m[u] == kEmpty) continue;
-            uint32_t slot = sl[u], k2 = kk[u], probes = 0;
-            while (k2 != m[u]) {
-              if (k2 == kEmpty) {
-                k2 = cas_u32(keys_s + 4 * slot, kEmpty, m[u]);
-                if (k2 == kEmpty) break;
-                continue;                                           // re-test the winner's key
-              }
+            if (!val[u]) continue;
+            uint32_t slot = sl[u], probes = 0, k2;
+            do {
               if (++probes > kProbeCap) { full = true; break; }
               slot = (slot + 1) & hmask;
               k2 = lds_u32(keys_s + 4 * slot);
-            }
-            if (!full) red_add_u32(acc_s + 4 * slot, b4 + u * 32 + lane >= sj ? ad_j : as_j);
+              if (k2 == kEmpty) {
+                k2 = cas_u32(keys_s + 4 * slot, kEmpty, m[u]);
+                if (k2 == kEmpty) break;
+              }
+            } while (k2 != m[u]);
+            if (!full) red_add_u32(acc_s + 4 * slot, add[u]);
           }
-          if (__any_sync(0xFFFFFFFFu, full)) { stop = true; break; }
         }
       }
+      if (full) s_full = 1;
+      __syncthreads();                                             // rows are rewritten by the next tile
+      if (s_full) break;
     }
-    if (stop && lane == 0) s_defer = 1;
+    // ---- phase 2a: dense list of the occupied slots (but n's): S / THREADS (<= 64) slots per thread
+    uint64_t occ = 0;
+    {
+      const uint32_t per = S / THREADS, s0 = tid * per;
+      for (uint32_t j = 0; j < per; j += 4) {
+        const uint4 kv = *reinterpret_cast<const uint4 *>(keys + s0 + j);
+        occ |= (uint64_t)((uint32_t)(kv.x != kEmpty) | (uint32_t)(kv.y != kEmpty) << 1 |
+                          (uint32_t)(kv.z != kEmpty) << 2 | (uint32_t)(kv.w != kEmpty) << 3) << j;
+      }
+      if (s_self - s0 < per) occ &= ~(1ull << (s_self - s0));
+    }
+    const uint32_t c1 = __popcll(occ), ci = warp_incl_scan(c1);
+    if (lane == 31) s_wsum[w] = ci;
     __syncthreads();
-    if (s_defer) {
-      if (tid == 0) F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
+    uint32_t woff = 0, count = 0;
+#pragma unroll
+    for (uint32_t q = 0; q < NW; ++q) { const uint32_t x = s_wsum[q]; woff += q < w ? x : 0u; count += x; }
+    if (s_full || count > ucap) {                                  // table too small: next tier
       __syncthreads();
-      continue;
+      if (tid == 0) F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
+      for (uint32_t i = tid; i < S / 4; i += THREADS) {
+        reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        reinterpret_cast<uint4 *>(acc)[i] = make_uint4(0, 0, 0, 0);
+      }
+      continue;                                                    // phase 0's barrier orders the clear
     }
-    // ---- phase 2a: compact the occupied slots (but n's) into a dense list. Each warp owns a
-    // contiguous range of the table: pass 1 counts (ballots), a warp-level prefix gives offsets,
-    // pass 2 writes — no atomics, conflict-free 32-slot sweeps.
-    const uint32_t lt = (1u << lane) - 1;
-    const uint32_t per_w = S / NW, w0 = w * per_w;
-    uint32_t mine = 0;
-    for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
-      const uint32_t v = keys[sb + lane];
-      mine += __popc(__ballot_sync(0xFFFFFFFFu, v != kEmpty && v != n));
+    {
+      uint32_t pos = woff + ci - c1;
+      uint64_t x = occ;
+      const uint32_t s0 = tid * (S / THREADS);
+      while (x) {
+        const uint32_t j = __ffsll((long long)x) - 1;
+        x &= x - 1;
+        ulist[pos++] = (uint16_t)(s0 + j);
+      }
     }
-    if (lane == 0) s_wcnt[w] = mine;
-    __syncthreads();
+    // ---- phase 2b: pool space for N(n), then validity / flags / noise / top-pi
     if (tid == 0) {
-      uint32_t acc0 = 0;
-      for (uint32_t q = 0; q < NW; ++q) { const uint32_t c1 = s_wcnt[q]; s_wcnt[q] = acc0; acc0 += c1; }
-      s_count = acc0;
-      if (acc0 > S / 2) {                                         // the dense list holds S/2 entries
+      s_defer = 0;
+      const unsigned long long st = atomicAdd(F.pool_cursor, (unsigned long long)count);
+      s_start = st;
+      F.cnt[n - J.lo] = count;
+      if (st + count > F.pool_cap) {
         s_defer = 1;
-        F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
+        F.pool_list[atomicAdd(F.pool_count, 1u)] = n;
       } else {
-        const unsigned long long st = atomicAdd(F.pool_cursor, (unsigned long long)acc0);
-        s_start = st;
-        if (st + acc0 > F.pool_cap) {
-          s_defer = 1;
-          F.cnt[n - J.lo] = acc0;
-          F.pool_list[atomicAdd(F.pool_count, 1u)] = n;
-        }
+        F.start[n - J.lo] = st + F.start_bias;
       }
     }
     __syncthreads();
-    if (s_defer) { __syncthreads(); continue; }
-    uint32_t wpos = s_wcnt[w];
-    for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
-      const uint32_t v = keys[sb + lane];
-      const bool has = v != kEmpty && v != n;
-      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, has);
-      if (has) ulist[wpos + __popc(bal & lt)] = sb + lane;
-      wpos += __popc(bal);
+    if (!s_defer) {
+      if (s_small) eval_top<PIMAX, THREADS, true>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
+      else eval_top<PIMAX, THREADS, false>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
     }
     __syncthreads();
-    const uint32_t count = s_count;
-    // ---- phase 2b: validity (Eq.6), flags, the N(n) entries with their flags,
-    // noise, per-thread top-pi; phase 3: top-pi merge (warps, then warp 0)
-    if (tid == 0) F.start[n - J.lo] = s_start + F.start_bias;
-    if (tid == 0) F.cnt[n - J.lo] = count;
-    if (s_small) eval_top<PIMAX, THREADS, true>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
-    else eval_top<PIMAX, THREADS, false>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
-    __syncthreads();
+    // ---- reset the used slots
+    for (uint32_t i = tid; i < count; i += THREADS) {
+      const uint32_t sl = ulist[i];
+      keys[sl] = kEmpty;
+      acc[sl] = 0;
+    }
+    if (tid == 0) { keys[s_self] = kEmpty; acc[s_self] = 0; }
   }
 }
 
@@ -302,6 +394,13 @@ __global__ void k_fused_pack(const uint32_t *pool, const uint64_t *start, const 
   if (lane == 0) atomicMax(maxdeg, mx);
 }
 
+__global__ void k_edge_cv(const uint64_t *edge_off, const uint32_t *edge_w, uint32_t E, uint32_t norm, uint64_t *cv) {
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const uint64_t we = (uint64_t)edge_w[e] << HGP_FP_SHIFT;   // Eq.5 term c(e), 2^-24 fixed point
+    cv[e] = norm ? we : we / (edge_off[e + 1] - edge_off[e]);
+  }
+}
+
 __global__ void k_pairs_total(const uint64_t *edge_off, uint32_t E, unsigned long long *T) {
   uint64_t s = 0;
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
@@ -315,7 +414,7 @@ __global__ void k_pairs_total(const uint64_t *edge_off, uint32_t E, unsigned lon
 // tiers of the fused kernel: A 4096 slots (40 KB incl. the dense list) for every node, M 8192
 // slots (72 KB, 3 CTAs/SM), B 16384 slots (144 KB, 1 CTA/SM); what B cannot hold (or the packed
 // accumulator cannot represent) goes to the unfused kernels.
-static constexpr uint32_t kFALog = 12, kFMLog = 13, kFBLog = 14;
+static constexpr int kFALog = 12, kFMLog = 13, kFBLog = 14;
 static constexpr uint32_t kFMThreads = 256, kFBThreads = 256;
 
 struct TierLists {
@@ -325,39 +424,37 @@ struct TierLists {
   uint32_t *ld, *cd;                    // B -> unfused (appended)
 };
 
-constexpr uint32_t fused_smem(uint32_t lg) { return (8u << lg) + (2u << (lg - 1)); }
 
 template <int PIMAX, int TA, int MINB>
 hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_nbrscore<TA, PIMAX, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused_smem(kFALog));
-    cudaFuncSetAttribute(k_nbrscore<kFMThreads, PIMAX, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_nbrscore<TA, PIMAX, MINB, kFALog>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused_smem(kFALog));
+    cudaFuncSetAttribute(k_nbrscore<kFMThreads, PIMAX, 3, kFMLog>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          fused_smem(kFMLog));
-    cudaFuncSetAttribute(k_nbrscore<kFBThreads, PIMAX, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_nbrscore<kFBThreads, PIMAX, 1, kFBLog>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          fused_smem(kFBLog));
     attr = true;
   }
   const uint32_t sm = c->sm_count;
   F.list = L.in_list; F.list_count = L.in_count; F.log2s = kFALog;
   F.defer_list = L.la; F.defer_count = L.ca;
-  const uint32_t per_sm = TA == 128 ? 32u : 16u;
+  const uint32_t per_sm = MINB;                                     // exactly the resident CTAs
   const uint32_t gA = L.hn < per_sm * sm ? L.hn : per_sm * sm;
   if (gA == 0) return HGP_OK;
-  HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
+  HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
   F.list = L.la; F.list_count = L.ca; F.log2s = kFMLog;
   F.defer_list = L.lm; F.defer_count = L.cm;
-  HGP_TRY(launch(c, "nbrscore_M", k_nbrscore<kFMThreads, PIMAX, 3>, dim3(3 * sm), dim3(kFMThreads), fused_smem(kFMLog), F));
+  HGP_TRY(launch(c, "nbrscore_M", k_nbrscore<kFMThreads, PIMAX, 3, kFMLog>, dim3(3 * sm), dim3(kFMThreads), fused_smem(kFMLog), F));
   F.list = L.lm; F.list_count = L.cm; F.log2s = kFBLog;
   F.defer_list = L.ld; F.defer_count = L.cd;
-  HGP_TRY(launch(c, "nbrscore_B", k_nbrscore<kFBThreads, PIMAX, 1>, dim3(sm), dim3(kFBThreads), fused_smem(kFBLog), F));
+  HGP_TRY(launch(c, "nbrscore_B", k_nbrscore<kFBThreads, PIMAX, 1, kFBLog>, dim3(sm), dim3(kFBThreads), fused_smem(kFBLog), F));
   return HGP_OK;
 }
 
 template <int PIMAX>
 hgp_status fused_tiers(hgp_ctx *c, FusedJob F, const TierLists &L) {
   static const int cfg = getenv("HGP_FUSED_CFG") ? atoi(getenv("HGP_FUSED_CFG")) : 1;
-  if (cfg == 1) return fused_tiers_t<PIMAX, 256, 6>(c, F, L);
   if (cfg == 2) return fused_tiers_t<PIMAX, 256, 4>(c, F, L);
   return fused_tiers_t<PIMAX, 256, 5>(c, F, L);
 }
@@ -416,8 +513,13 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   uint32_t *LA = lists, *LM = lists + nn, *LD = lists + 2 * (size_t)nn, *LP = lists + 3 * (size_t)nn;
   // counts: 0 A->M, 1 M->B, 2 deferred (unfused), 3 pool overflow, 4/5 second pass A->M / M->B,
   // 6 second-pass pool overflow (impossible: exact pool), 7 max degree
+  uint64_t *cv = scratch_raw<uint64_t>(c, g->E ? g->E : 1, &st);
+  if (st) return st;
+  HGP_TRY(launch(c, "edge_cv", k_edge_cv, dim3(g->E ? (div_up(g->E, 256) < 4096 ? div_up(g->E, 256) : 4096) : 0), dim3(256), 0,
+                 (const uint64_t *)g->edge_off, (const uint32_t *)g->edge_w, g->E, p->norm, cv));
   FusedJob F{};
   F.S = J;
+  F.cv = cv;
   F.pool = pool; F.pool_cap = pool_cap; F.pool_cursor = misc + 1; F.start = start; F.cnt = cnt;
   F.pool_list = LP; F.pool_count = counts + 3;
   TierLists L{nullptr, nullptr, nn, LA, counts + 0, LM, counts + 1, LD, counts + 2};
