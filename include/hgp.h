@@ -53,6 +53,7 @@ extern "C" {
 #define HGP_FP_SHIFT 24
 #define HGP_PURGE 0x80000000u             /* neighbour entry flag: permanently invalid */
 #define HGP_MAX_PI 16
+#define HGP_MAX_LEVELS 64   /* hgp_coarsen: at most this many levels */
 
 typedef enum {
   HGP_OK = 0,
@@ -212,6 +213,21 @@ HGP_API hgp_status hgp_shard_bounds(hgp_ctx *ctx, const hgp_csr *g, uint32_t wor
 HGP_API hgp_status hgp_coarsen_level0(hgp_ctx *ctx, const hgp_csr *g, const hgp_params *p, hgp_cand *cand,
                                       uint32_t *match, uint32_t *gamma, hgp_nbrs *nb, hgp_csr *coarse,
                                       hgp_nbrs *coarse_nb, hgp_level_stats *stats);
+
+/* Multi-level coarsening driver (paper §5): level 0 by
+ * hgp_coarsen_level0, level l >= 1 by hgp_coarsen_level on the previous coarse CSR and coarse
+ * neighbour lists, noise seed p->noise_seed + l (reading #3). Stops after the first level whose
+ * coarse node count is <= ceil(W / Omega) (1 if Omega = HGP_UNBOUNDED; W = total size) or that
+ * matched no pair (reading #20), or after max_levels (1..HGP_MAX_LEVELS) levels.
+ *   rho        caller DEVICE [g0->N]: rho = gamma^L o ... o gamma^1, each level-0 node's node on
+ *              the coarsest level (the initial partition's clusters)
+ *   coarsest, coarsest_nb   library-owned coarsest level (free with hgp_csr_free / hgp_nbrs_free)
+ *   stats      HOST [max_levels] per-level stats, or NULL; *levels_out = L (number of levels run)
+ * g0 is borrowed and left unchanged. Errors of a level are returned as is (nothing is
+ * allocated on error). Synchronises. */
+HGP_API hgp_status hgp_coarsen(hgp_ctx *ctx, const hgp_csr *g0, const hgp_params *p, uint32_t max_levels,
+                               uint32_t *rho, hgp_csr *coarsest, hgp_nbrs *coarsest_nb, hgp_level_stats *stats,
+                               uint32_t *levels_out);
 
 HGP_API void hgp_csr_free(hgp_ctx *ctx, hgp_csr *g);
 HGP_API void hgp_nbrs_free(hgp_ctx *ctx, hgp_nbrs *nb);

@@ -278,8 +278,7 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
       reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     __syncthreads();
     // 4 entries per thread in flight: nbr loads, then the gamma gathers, then the inserts
-    for (uint64_t kb = tid - lane; kb < na + nbn; kb += 4 * THREADS) {   // warp-uniform trip count
-      const uint64_t k0 = kb + lane;
+    for (uint64_t k0 = tid; k0 < na + nbn; k0 += 4 * THREADS) {
       uint32_t v[4], gm[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -288,59 +287,27 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) gm[u] = v[u] != kEmpty ? __ldg(J.gamma + (v[u] & kIdMask)) : kEmpty;
-      if constexpr (SMEM) {
-        // fast path, straight-line and predicated: home slot load; an empty home is claimed with
-        // one CAS; a home holding gamma(m) gets the flag OR-ed in if needed. Keys displaced by a
-        // collision probe on (divergent, entered only when some lane of the warp needs it).
-        uint32_t sl[4], kk[4];
-        bool miss[4], anym = false;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          sl[u] = hash_slot(gm[u], log2s);
-          kk[u] = lds_u32(keys_s + 4 * sl[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const bool valid = v[u] != kEmpty;
-          const bool fl = (v[u] & kPurge) != 0;
-          purged += valid && fl;
-          const uint32_t key = fl ? (gm[u] | kPurge) : gm[u];
-          const bool claim = valid && kk[u] == kEmpty;
-          uint32_t old = kk[u];
-          if (claim) old = cas_u32(keys_s + 4 * sl[u], kEmpty, key);
-          const bool mine = claim && old == kEmpty;
-          const bool same = (old & kIdMask) == gm[u] && old != kEmpty;
-          if (valid && !mine && same && fl && !(old & kPurge))
-            asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(keys_s + 4 * sl[u]), "r"(kPurge) : "memory");
-          miss[u] = valid && !mine && !same;
-          anym |= miss[u];
-        }
-        if (__any_sync(0xFFFFFFFFu, anym)) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (!miss[u]) continue;
-            const bool fl = (v[u] & kPurge) != 0;
-            uint32_t slot = sl[u];
-            while (true) {
-              slot = (slot + 1) & hmask;
-              uint32_t k = lds_u32(keys_s + 4 * slot);
-              if (k == kEmpty) {
-                k = cas_u32(keys_s + 4 * slot, kEmpty, fl ? (gm[u] | kPurge) : gm[u]);
-                if (k == kEmpty) break;
-              }
-              if ((k & kIdMask) == gm[u]) {
-                if (fl && !(k & kPurge)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(keys_s + 4 * slot), "r"(kPurge) : "memory");
-                break;
-              }
+      for (int u = 0; u < 4; ++u) {
+        if (v[u] == kEmpty) continue;
+        const bool fl = (v[u] & kPurge) != 0;
+        purged += fl;
+        if constexpr (SMEM) {
+          uint32_t slot = hash_slot(gm[u], log2s);
+          uint32_t k = lds_u32(keys_s + 4 * slot);
+          while (true) {
+            if (k == kEmpty) {
+              k = cas_u32(keys_s + 4 * slot, kEmpty, fl ? (gm[u] | kPurge) : gm[u]);
+              if (k == kEmpty) break;
             }
+            if ((k & kIdMask) == gm[u]) {
+              if (fl && !(k & kPurge)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(keys_s + 4 * slot), "r"(kPurge) : "memory");
+              break;
+            }
+            slot = (slot + 1) & hmask;
+            k = lds_u32(keys_s + 4 * slot);
           }
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (v[u] == kEmpty) continue;
-          const bool fl = (v[u] & kPurge) != 0;
-          purged += fl;
+        } else {
           uint32_t slot;
           hs_insert_flagged(keys, log2s, gm[u], fl, &slot);
         }

@@ -282,7 +282,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
               " setp.eq.u32 ph, o, %4;\n"
               " setp.eq.or.u32 ph, o, -1, ph;\n"
               " and.pred ph, ph, pv;\n"
-              " @ph red.shared.add.u32 [%1+%6], %5;\n"
+              " selp.u32 o, %5, 0, ph;\n"                       // a miss adds 0 to the
+              " red.shared.add.u32 [%1+%6], o;\n"               // slot it looked at: no branch
               " not.pred ph, ph;\n"
               " and.pred ph, ph, pv;\n"
               " selp.u32 %0, 1, 0, ph;\n}"

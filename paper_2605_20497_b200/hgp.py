@@ -118,6 +118,9 @@ def lib():
                                    ctypes.POINTER(CNbrs)]
         L.hgp_coarsen_level.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.POINTER(CNbrs), ctypes.POINTER(CParams), vp,
                                         vp, vp, ctypes.POINTER(CCsr), ctypes.POINTER(CNbrs), ctypes.POINTER(CStats)]
+        L.hgp_coarsen.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.POINTER(CParams), ctypes.c_uint32, vp,
+                                  ctypes.POINTER(CCsr), ctypes.POINTER(CNbrs), vp, ctypes.POINTER(ctypes.c_uint32)]
+        L.hgp_coarsen.restype = S
         L.hgp_neighbors_and_scores.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.POINTER(CParams), ctypes.c_uint32,
                                                ctypes.c_uint32, ctypes.POINTER(CNbrs), vp]
         L.hgp_shard_bounds.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32)]
@@ -379,6 +382,21 @@ def coarsen_level0(ctx: Ctx, g: Csr, p: CParams, cand: torch.Tensor | None, matc
                                     _ptr(gamma), ctypes.byref(nb) if want_nbrs else None, ctypes.byref(oc),
                                     ctypes.byref(on), ctypes.byref(st)))
     return (Nbrs(ctx, nb) if want_nbrs else None), Csr(ctx, oc), Nbrs(ctx, on), st.as_dict(p.pi)
+
+
+MAX_LEVELS = 64
+
+
+def coarsen(ctx: Ctx, g: Csr, p: CParams, max_levels: int = MAX_LEVELS):
+    """Multi-level driver (hgp_coarsen): returns (rho [N0] u32 device tensor,
+    coarsest Csr, coarsest Nbrs, per-level stats dicts)."""
+    rho = torch.empty(g.N, dtype=torch.uint32, device="cuda")
+    oc, on = CCsr(), CNbrs()
+    st = (CStats * max_levels)()
+    nl = ctypes.c_uint32(0)
+    _check(lib().hgp_coarsen(ctx.h, ctypes.byref(g.c), ctypes.byref(p), max_levels, _ptr(rho), ctypes.byref(oc),
+                             ctypes.byref(on), ctypes.cast(st, vp), ctypes.byref(nl)))
+    return rho, Csr(ctx, oc), Nbrs(ctx, on), [st[i].as_dict(p.pi) for i in range(nl.value)]
 
 
 def cand_to_numpy(cand: torch.Tensor) -> np.ndarray:

@@ -1,6 +1,6 @@
 # quick GPU iteration: fused-path parity + bench (no e2e / cpu baseline)
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "fused or giant or level_steps" 2>&1 | tail -4 > gpurun_out/pytest_quick.log
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_multilevel.py -m gpu -x -q -k "fused or giant or level_steps or multilevel" 2>&1 | tail -4 > gpurun_out/pytest_quick.log
 cat gpurun_out/pytest_quick.log
 timeout 600 python bench.py --no-cpu-baseline --no-e2e ${BENCH_ARGS} > gpurun_out/bench_quick.json 2> gpurun_out/bench_quick.err
 tail -2 gpurun_out/bench_quick.err
