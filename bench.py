@@ -315,6 +315,29 @@ def main():
         e2e = {"value": P / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": 4 * N}
 
+    # ---- whole hierarchy: a1 + hgp_coarsen to the stop rule, 1 GPU, CUDA events
+    hier = None
+    if world == 1:
+        def hierarchy():
+            g = hgp.build_csr(ctx, N, dev["edge_off"], dev["edge_nsrc"], dev["pins"], dev["edge_w"], dev["node_w"])
+            rho, cg, cnb, levels = hgp.coarsen(ctx, g, params)
+            out = (levels, cg.N)
+            for x in (g, cg, cnb):
+                x.free()
+            return out
+        hierarchy()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        levels, n_last = hierarchy()
+        h1.record(stream)
+        torch.cuda.synchronize()
+        hms = h0.elapsed_time(h1)
+        hier = {"what": "a1 + every level to the stop rule (hgp_coarsen, reading #20)", "levels": len(levels),
+                "total_coarsening_ms": hms, "pins_per_s": P / (hms / 1e3), "coarsest_nodes": n_last,
+                "level_ms": [round(l["ms"]["total"], 3) for l in levels],
+                "level_nodes": [l["N"] for l in levels],
+                "matched_fraction": [round(2 * sum(l["matched_per_round"]) / max(l["N"], 1), 4) for l in levels]}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -359,6 +382,8 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    if hier:
+        line["hierarchy"] = hier
     if world == 1 and not args.no_cpu_baseline:
         hs, om, de, desc = oracle_sample(args.workload, args.seed, "baseline")
         t = oracle_level_seconds(hs, om, de, pi, hgpgen.default_noise_cap(hs), args.seed)

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // build_csr.cu — a1: validate the problem statement and materialise the
 // compressed sparse level: canonical hyperedges (src block ascending, dst block
 // ascending) and the transposed incidence (in(n) ascending, then out(n) ascending), with
@@ -169,6 +170,8 @@ struct IncBlockSeg {   // segment 2n = in(n), 2n+1 = out(n)
 // Given edge_off/edge_nsrc/pins/edge_mu of g (device), allocate and fill inc_off, inc_nin,
 // inc, in_mu and g->max_inc. Synchronises (reads max degree).
 hgp_status build_incidence(hgp_ctx *c, hgp_csr *g) {
+  static const bool atomic_path = getenv("HGP_INC_ATOMIC") != nullptr;   // A/B switch (measurement)
+  if (!atomic_path && g->P < (1ull << 30) && g->N < (1u << 30)) return build_incidence_radix(c, g);
   hgp_status st = HGP_OK;
   const uint32_t N = g->N, E = g->E;
   const uint64_t P = g->P;

@@ -100,17 +100,19 @@ template <class K, class... Args>
 inline hgp_status launch(hgp_ctx *c, const char *name, K kernel, dim3 grid, dim3 block, size_t smem,
                          Args... args) {
   if (grid.x == 0 || grid.y == 0 || grid.z == 0) return HGP_OK;
-  const bool prof = c->prof_on && strstr(name, c->prof_filter.c_str()) != nullptr;
+  static const bool dbg = getenv("HGP_DEBUG_SYNC") != nullptr;   // debugging: serialise + trace
+  const bool prof = (c->prof_on && strstr(name, c->prof_filter.c_str()) != nullptr) || dbg;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (prof) { e0 = c->prof_event(); e1 = c->prof_event(); cudaEventRecord(e0, c->stream); }
   kernel<<<grid, block, smem, c->stream>>>(args...);
   if (prof) { cudaEventRecord(e1, c->stream); c->prof_events.push_back({e0, e1}); c->prof_names.push_back(name); }
   c->launches++;
-  static const bool dbg = getenv("HGP_DEBUG_SYNC") != nullptr;   // debugging: serialise + trace
   if (dbg) {
     fprintf(stderr, "[hgp] %s grid %u block %u smem %zu ...", name, grid.x, block.x, smem);
     cudaError_t se = cudaStreamSynchronize(c->stream);
-    fprintf(stderr, " %s\n", cudaGetErrorString(se));
+    float ms = -1.f;
+    if (e0) { cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1); }
+    fprintf(stderr, " %s %.3f ms\n", cudaGetErrorString(se), ms);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(HGP_E_CUDA, "launch %s: %s", name, cudaGetErrorString(e));

@@ -5,6 +5,8 @@
 namespace hgp {
 // Allocate and fill inc_off / inc_nin / inc / in_mu / max_inc of g from its edge arrays.
 hgp_status build_incidence(hgp_ctx *c, hgp_csr *g);
+// The same by a stable LSD radix sort of (pin << 1 | is_src, edge) pairs (radix.cu); P < 2^30.
+hgp_status build_incidence_radix(hgp_ctx *c, hgp_csr *g);
 void free_csr(hgp_ctx *c, hgp_csr *g);
 void free_nbrs(hgp_ctx *c, hgp_nbrs *nb);
 // Neighbour segments left in the fused kernel's pool (not compacted into a CSR): segment n is

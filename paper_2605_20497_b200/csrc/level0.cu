@@ -11,6 +11,7 @@
 // Nodes the packed form cannot represent, or whose neighbourhood overflows the largest shared
 // table, are handled by the unfused kernels (list mode, over the same segment view).
 #include <cstdlib>
+#include <type_traits>
 
 #include "csr_impl.cuh"
 #include "hashset.cuh"
@@ -48,6 +49,7 @@ __device__ __forceinline__ void eval_top(const ScoreJob &J, const FusedJob &F, u
   TopK<PIMAX> topk;
 #pragma unroll
   for (int i = 0; i < PIMAX; ++i) { top.s[i] = 0; top.id[i] = 0; topk.k[i] = 0; }
+  uint64_t thr = 0;                                                // topk.k[pi - 1]
   const uint64_t wn = J.node_w[n];
   const uint32_t inn = J.in_mu[n];
   const uint32_t imask = ib ? (uint32_t)((1ull << ib) - 1) : 0u;
@@ -66,8 +68,17 @@ __device__ __forceinline__ void eval_top(const ScoreJob &J, const FusedJob &F, u
       const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
       sc += __umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);   // uniform in [0, cap]
     }
-    if (PACKED) topk_insert<PIMAX>(topk, J.pi, (sc << 32) | v);
-    else top_insert<PIMAX>(top, J.pi, sc, v);
+    if (PACKED) {
+      const uint64_t key = (sc << 32) | v;
+      if (key > thr) {                                             // most candidates stop here
+        topk_insert<PIMAX>(topk, J.pi, key);
+#pragma unroll
+        for (int q = 0; q < PIMAX; ++q)
+          if (q == (int)J.pi - 1) thr = topk.k[q];
+      }
+    } else {
+      top_insert<PIMAX>(top, J.pi, sc, v);
+    }
   }
   if (PACKED) warp_topk_merge<PIMAX>(topk, J.pi, s_tops + w * PIMAX);
   else warp_top_merge<PIMAX>(top, J.pi, s_tops + w * PIMAX, s_topi + w * PIMAX);
@@ -147,8 +158,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
   __shared__ uint32_t s_topi[(NW + 1) * PIMAX];
   __shared__ uint64_t s_sum[NW], s_g[NW];
   __shared__ uint32_t s_wsum[NW];
-  __shared__ uint32_t s_defer, s_ib, s_small, s_full, s_self;
-  __shared__ uint64_t s_gcd;
+  __shared__ uint32_t s_defer, s_full, s_self;
   __shared__ unsigned long long s_start;
   const ScoreJob &J = F.S;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -168,9 +178,19 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
     const uint32_t n = F.list ? F.list[t] : J.lo + t;
     const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1], iin = i0 + J.inc_nin[n];
     const uint32_t inn = J.in_mu[n];
-    // ---- phase 0
-    uint64_t sum = 0, gg = 0;
-    for (uint64_t k = i0 + tid; k < i1; k += THREADS) {
+    // ---- phase 0: sum / gcd of c(e) over I(n); the first tile's edge data stays in registers
+    uint32_t te = 0, tlen = 0, tns = 0, tmu = 0;
+    uint64_t ta = 0, tce = 0;
+    if (tid < kKT && i0 + tid < i1) {
+      te = J.inc[i0 + tid];
+      ta = J.edge_off[te];
+      tlen = (uint32_t)(J.edge_off[te + 1] - ta);
+      tns = J.edge_nsrc[te];
+      tce = F.cv[te];
+      tmu = i0 + tid < iin ? J.edge_mu[te] : 0u;
+    }
+    uint64_t sum = tce, gg = tce;
+    for (uint64_t k = i0 + kKT + tid; k < i1; k += THREADS) {
       const uint64_t ce = F.cv[J.inc[k]];
       sum += ce;
       gg = gcd64(gg, ce);
@@ -183,43 +203,47 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
     }
     if (lane == 0) { s_sum[w] = sum; s_g[w] = gg; }
     __syncthreads();   // also: the table is clean (initial clear / previous node's reset)
-    if (tid == 0) {
-      uint64_t S1 = 0, G1 = 0;
-      for (uint32_t q = 0; q < NW; ++q) { S1 += s_sum[q]; G1 = gcd64(G1, s_g[q]); }
-      if (G1 == 0) G1 = 1;
-      const uint32_t bits = inn ? 32 - __clz(inn) : 0;
-      const unsigned __int128 need = ((unsigned __int128)(S1 / G1 + 1)) << bits;
-      s_defer = need > ((unsigned __int128)1 << 32);
-      s_gcd = G1;
-      s_ib = bits;
-      s_small = (unsigned __int128)S1 + J.noise_cap < ((unsigned __int128)1 << 32);
-      s_full = 0;
-      if (!s_defer) {
-        bool ins = false;
-        s_self = hs_insert_slot(keys, log2s, n, &ins);            // self-visits land in n's slot
-      }
+    uint64_t S1 = 0, g = 0;                                        // every thread, same values
+#pragma unroll
+    for (uint32_t q = 0; q < NW; ++q) {
+      S1 += s_sum[q];
+      const uint64_t x = s_g[q];
+      if (x != g) g = gcd64(g, x);
     }
-    __syncthreads();
-    if (s_defer) {
+    if (g == 0) g = 1;
+    const uint32_t ib = inn ? 32 - __clz(inn) : 0;
+    const bool small = (unsigned __int128)S1 + J.noise_cap < ((unsigned __int128)1 << 32);
+    if ((((unsigned __int128)(S1 / g + 1)) << ib) > ((unsigned __int128)1 << 32)) {   // packed form inexact
       if (tid == 0) F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
-      __syncthreads();
+      __syncthreads();                                             // s_sum / s_g are rewritten next
       continue;
     }
-    const uint64_t g = s_gcd;
-    const uint32_t ib = s_ib;
+    if (tid == 0) {
+      s_full = 0;
+      bool ins = false;
+      s_self = hs_insert_slot(keys, log2s, n, &ins);              // self-visits land in n's slot
+    }
+    if (i1 == i0) __syncthreads();                                 // no tile barrier orders s_self
     // ---- phase 1, tile by tile
     for (uint64_t t0 = i0; t0 < i1; t0 += kKT) {
       const uint32_t kt = (uint32_t)min((uint64_t)kKT, i1 - t0);
       uint32_t len = 0, ns = 0, as = 0, ad = 0;
       uint64_t a = 0;
       if (tid < kt) {
-        const uint32_t e = J.inc[t0 + tid];
-        a = J.edge_off[e];
-        len = (uint32_t)(J.edge_off[e + 1] - a);
-        ns = J.edge_nsrc[e];
-        const uint64_t ce = F.cv[e];
+        uint64_t ce = tce;
+        uint32_t mu = tmu;
+        if (t0 == i0) {
+          a = ta; len = tlen; ns = tns;
+        } else {
+          const uint32_t e = J.inc[t0 + tid];
+          a = J.edge_off[e];
+          len = (uint32_t)(J.edge_off[e + 1] - a);
+          ns = J.edge_nsrc[e];
+          ce = F.cv[e];
+          mu = t0 + tid < iin ? J.edge_mu[e] : 0u;
+        }
         as = (uint32_t)((ce == g ? 1ull : ce / g) << ib);
-        ad = as + (t0 + tid < iin ? J.edge_mu[e] : 0u);           // m in dst(e), e in in(n)
+        ad = as + mu;                                              // m in dst(e), e in in(n)
       }
       const uint32_t incl = warp_incl_scan(len);
       if (lane == 31) s_wsum[w] = incl;
@@ -316,17 +340,19 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       if (s_full) break;
     }
     // ---- phase 2a: dense list of the occupied slots (but n's): S / THREADS (<= 64) slots per thread
-    uint64_t occ = 0;
-    {
-      const uint32_t per = S / THREADS, s0 = tid * per;
-      for (uint32_t j = 0; j < per; j += 4) {
-        const uint4 kv = *reinterpret_cast<const uint4 *>(keys + s0 + j);
-        occ |= (uint64_t)((uint32_t)(kv.x != kEmpty) | (uint32_t)(kv.y != kEmpty) << 1 |
-                          (uint32_t)(kv.z != kEmpty) << 2 | (uint32_t)(kv.w != kEmpty) << 3) << j;
-      }
-      if (s_self - s0 < per) occ &= ~(1ull << (s_self - s0));
+    constexpr uint32_t kPer = S / THREADS;
+    using Occ = typename std::conditional<(kPer <= 32), uint32_t, uint64_t>::type;
+    Occ occ = 0;
+    const uint32_t s0 = tid * kPer;
+#pragma unroll
+    for (uint32_t j = 0; j < kPer; j += 4) {
+      const uint4 kv = *reinterpret_cast<const uint4 *>(keys + s0 + j);
+      occ |= (Occ)((uint32_t)(kv.x != kEmpty) | (uint32_t)(kv.y != kEmpty) << 1 | (uint32_t)(kv.z != kEmpty) << 2 |
+                   (uint32_t)(kv.w != kEmpty) << 3)
+             << j;
     }
-    const uint32_t c1 = __popcll(occ), ci = warp_incl_scan(c1);
+    if (s_self - s0 < kPer) occ &= ~((Occ)1 << (s_self - s0));
+    const uint32_t c1 = sizeof(Occ) == 4 ? __popc((uint32_t)occ) : __popcll((uint64_t)occ), ci = warp_incl_scan(c1);
     if (lane == 31) s_wsum[w] = ci;
     __syncthreads();
     uint32_t woff = 0, count = 0;
@@ -343,10 +369,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
     }
     {
       uint32_t pos = woff + ci - c1;
-      uint64_t x = occ;
-      const uint32_t s0 = tid * (S / THREADS);
+      Occ x = occ;
       while (x) {
-        const uint32_t j = __ffsll((long long)x) - 1;
+        const uint32_t j = sizeof(Occ) == 4 ? __ffs((int)(uint32_t)x) - 1 : __ffsll((long long)x) - 1;
         x &= x - 1;
         ulist[pos++] = (uint16_t)(s0 + j);
       }
@@ -366,7 +391,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
     }
     __syncthreads();
     if (!s_defer) {
-      if (s_small) eval_top<PIMAX, THREADS, true>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
+      if (small) eval_top<PIMAX, THREADS, true>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
       else eval_top<PIMAX, THREADS, false>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
     }
     __syncthreads();
@@ -456,8 +481,8 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
 template <int PIMAX>
 hgp_status fused_tiers(hgp_ctx *c, FusedJob F, const TierLists &L) {
   static const int cfg = getenv("HGP_FUSED_CFG") ? atoi(getenv("HGP_FUSED_CFG")) : 1;
-  if (cfg == 2) return fused_tiers_t<PIMAX, 256, 4>(c, F, L);
-  return fused_tiers_t<PIMAX, 256, 5>(c, F, L);
+  if (cfg == 3) return fused_tiers_t<PIMAX, 256, 5>(c, F, L);   // 48 registers, 5 CTAs/SM
+  return fused_tiers_t<PIMAX, 256, 4>(c, F, L);                   // 64 registers, 4 CTAs/SM (measured faster)
 }
 
 __global__ void k_list_cnt_sum(const uint32_t *list, const uint32_t *count, const uint32_t *cnt, uint32_t lo,

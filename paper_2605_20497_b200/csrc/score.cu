@@ -18,7 +18,10 @@ namespace hgp {
 // One CTA per node. MODE kModeP32: one u32 per bin packs (eta/g) << ib | inter, where g is the
 // gcd of the node's c(e) and ib = bits(in_mu(n)) (exact: inter <= in_mu(n) < 2^ib, and the
 // node qualifies only if (sum c / g + 1) << ib <= 2^32); a single native shared-memory atomic
-// add per pin visit. MODE kModeWide: u64 eta + u32 inter per bin.
+// add per pin visit. MODE kModeSplit: u32 eta + u32 inter per bin (exact when sum c(e) over I(n)
+// < 2^32: the usual case once hyperedge sizes differ and the gcd is 1); two native atomics per
+// visit (the inter one only for dst pins of in-edges). MODE kModeWide: u64 eta (CAS loop) + u32
+// inter per bin, for everything else.
 template <int THREADS, int MODE, bool SMEM, int PIMAX>
 __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -31,11 +34,12 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
   constexpr uint32_t NW = THREADS / 32;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t log2s = J.log2s, S = 1u << log2s;
-  constexpr uint32_t SLOT = MODE == kModeP32 ? 8 : 16;
+  constexpr uint32_t SLOT = MODE == kModeP32 ? 8 : MODE == kModeSplit ? 12 : 16;
   unsigned char *base = SMEM ? dyn : reinterpret_cast<unsigned char *>(J.gtab) + ((size_t)blockIdx.x * SLOT << log2s);
   uint32_t *keys = reinterpret_cast<uint32_t *>(base);
   uint32_t *acc = reinterpret_cast<uint32_t *>(base + ((size_t)4 << log2s));        // P32 acc / wide inter
   uint64_t *eta = reinterpret_cast<uint64_t *>(base + ((size_t)8 << log2s));        // wide only
+  uint32_t *inter32 = reinterpret_cast<uint32_t *>(base + ((size_t)8 << log2s) + 16);  // split only (S+1 slots)
   const uint32_t total = J.list_count ? *J.list_count : J.hi - J.lo;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = J.list ? J.list[t] : J.lo + t;
@@ -83,26 +87,47 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
       g = s_gcd;
       ib = s_ib;
     }
+    if (MODE == kModeSplit) {                                     // eta fits u32 iff sum c(e) < 2^32
+      uint64_t sum = 0;
+      for (uint64_t k = i0 + tid; k < i1; k += THREADS) {
+        const uint32_t e = J.inc[k];
+        sum += edge_c(J, e, J.edge_off[e], J.edge_off[e + 1]);
+      }
+      sum = warp_sum(sum);
+      if (lane == 0) s_sum[w] = sum;
+      __syncthreads();
+      uint64_t S1 = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < NW; ++q) S1 += s_sum[q];
+      __syncthreads();                                            // s_sum is rewritten next node
+      if (S1 >= (1ull << 32)) {                                   // CTA-uniform
+        if (tid == 0) J.wide_list[atomicAdd(J.wide_count, 1u)] = n;
+        continue;
+      }
+    }
     // ---- phase 1: bins = unflagged neighbours (+ n itself in P32 mode: every self-visit then
     // hits a real slot, no per-pin test; misses of purged neighbours go to a trash slot S)
     for (uint32_t i = tid; i < S; i += THREADS) {
       keys[i] = kEmpty;
       acc[i] = 0;
       if (MODE == kModeWide) eta[i] = 0;
+      if (MODE == kModeSplit) inter32[i] = 0;
     }
-    if (MODE == kModeP32 && tid == 0) acc[S] = 0;
+    if (MODE != kModeWide && tid == 0) acc[S] = 0;
+    if (MODE == kModeSplit && tid == 0) inter32[S] = 0;
     __syncthreads();
     for (uint64_t k = b0 + tid; k < b1; k += THREADS) {
       const uint32_t v = J.nbr[k];
       if (!(v & kPurge)) hs_insert(keys, log2s, v);
     }
-    if (MODE == kModeP32 && tid == 0) hs_insert(keys, log2s, n);
+    if (MODE != kModeWide && tid == 0) hs_insert(keys, log2s, n);
     __syncthreads();
     // ---- phase 2: traverse I(n): a warp loads the metadata of 32 incident edges at
     // once (lane = edge), then walks them; pins are fetched 128 at a time (4 per lane in flight).
     // Incident edges are dealt round-robin to warps (edge i0 + w + NW*l, l = 0, 1, ...): balanced.
     const uint32_t keys_s = opaque_u32(smem_u32addr(keys)), acc_s = opaque_u32(smem_u32addr(acc));
-    const uint32_t hmask = S - 1, hshift = 32u - log2s;
+    const uint32_t inter_s = MODE == kModeSplit ? smem_u32addr(inter32) : 0u;
+    const uint32_t hmask = S - 1;
     for (uint64_t kb = i0 + w; kb < i1; kb += (uint64_t)NW * 32) {
       const uint64_t k = kb + (uint64_t)NW * lane;
       uint64_t a = 0, ce = 0;
@@ -120,6 +145,9 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
       if (MODE == kModeP32) {
         add_s = (uint32_t)((ce / g) << ib);
         add_d = add_s + mu_in;                                     // m in dst(e) and e in in(n)
+      } else if (MODE == kModeSplit) {
+        add_s = (uint32_t)ce;                                      // eta term
+        add_d = mu_in;                                             // inter term of a dst pin
       }
       const uint32_t cnt = (uint32_t)min((uint64_t)32, (i1 - kb + NW - 1) / NW);
       for (uint32_t j = 0; j < cnt; ++j) {
@@ -128,7 +156,7 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
         const uint32_t sj = __shfl_sync(0xFFFFFFFFu, srel, j);
         uint32_t as_j = 0, ad_j = 0, mu_j = 0;
         uint64_t ce_j = 0;
-        if (MODE == kModeP32) {
+        if (MODE != kModeWide) {
           as_j = __shfl_sync(0xFFFFFFFFu, add_s, j);
           ad_j = __shfl_sync(0xFFFFFFFFu, add_d, j);
         } else {
@@ -143,7 +171,7 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
             const uint32_t idx = b4 + u * 32 + lane;
             m[u] = idx < lj ? __ldg(pj + idx) : kEmpty;
           }
-          if constexpr (MODE == kModeP32) {
+          if constexpr (MODE != kModeWide) {
             // first probes of the 4 pins issued back to back (ILP), collisions resolved after
             uint32_t sl[4], kk[4];
 #pragma unroll
@@ -164,7 +192,12 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
                 }
               }
               const bool dst = b4 + u * 32 + lane >= sj;
-              red_add_u32(acc_s + 4 * slot, dst ? ad_j : as_j);
+              if constexpr (MODE == kModeP32) {
+                red_add_u32(acc_s + 4 * slot, dst ? ad_j : as_j);
+              } else {
+                red_add_u32(acc_s + 4 * slot, as_j);
+                if (dst && ad_j) red_add_u32(inter_s + 4 * slot, ad_j);
+              }
             }
             continue;
           }
@@ -199,6 +232,9 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
         const uint32_t x = acc[slot];
         e_nm = (uint64_t)(ib < 32 ? x >> ib : 0) * g;
         inter = x & imask;
+      } else if (MODE == kModeSplit) {
+        e_nm = acc[slot];
+        inter = inter32[slot];
       } else {
         e_nm = eta[slot];
         inter = acc[slot];
@@ -261,6 +297,7 @@ __global__ void k_score_check(const uint32_t *node_w, const uint32_t *in_mu, uin
 static constexpr uint32_t kSALog = 12, kSAThreads = 128;
 static constexpr uint32_t kSBLog = 14, kSBThreads = 256;
 static constexpr uint32_t kSWLog = 12, kSWThreads = 256;
+static constexpr uint32_t kSSLog = 12, kSSThreads = 256;   // split tier: 48 KB, 4 CTAs/SM
 
 template <int PIMAX>
 hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_deg, uint32_t *lists,
@@ -274,6 +311,8 @@ hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_
                          (8 << kSBLog) + 16);
     cudaFuncSetAttribute(k_score<kSWThreads, kModeWide, true, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          16 << kSWLog);
+    cudaFuncSetAttribute(k_score<kSSThreads, kModeSplit, true, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (12 << kSSLog) + 32);
     attr = true;
   }
   uint32_t *bigA = lists, *wide = lists + nn, *huge = lists + 2 * (size_t)nn;
@@ -289,8 +328,14 @@ hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_
     HGP_TRY(launch(c, "score_B", k_score<kSBThreads, kModeP32, true, PIMAX>, dim3(c->sm_count), dim3(kSBThreads),
                    (8u << kSBLog) + 16, J));
   }
-  // W: nodes whose packed sums could overflow 32 bits (neighbourhoods up to 2048)
-  J.list = wide; J.list_count = counts + 1; J.cap = 1u << (kSWLog - 1); J.log2s = kSWLog;
+  // S: nodes whose packed sums could overflow 32 bits but whose eta fits u32 (split accumulators)
+  uint32_t *wide2 = lists + 3 * (size_t)nn;
+  J.list = wide; J.list_count = counts + 1; J.cap = 1u << (kSSLog - 1); J.log2s = kSSLog;
+  J.big_list = huge; J.big_count = counts + 2; J.wide_list = wide2; J.wide_count = counts + 3;
+  HGP_TRY(launch(c, "score_S", k_score<kSSThreads, kModeSplit, true, PIMAX>, dim3(4 * c->sm_count), dim3(kSSThreads),
+                 (12u << kSSLog) + 32, J));
+  // W: the rest (neighbourhoods up to 2048)
+  J.list = wide2; J.list_count = counts + 3; J.cap = 1u << (kSWLog - 1); J.log2s = kSWLog;
   J.big_list = huge; J.big_count = counts + 2;
   HGP_TRY(launch(c, "score_W", k_score<kSWThreads, kModeWide, true, PIMAX>, dim3(c->sm_count), dim3(kSWThreads),
                  16u << kSWLog, J));
@@ -369,7 +414,7 @@ hgp_status score_run(hgp_ctx *c, const hgp_csr *g, hgp_nbrs *nb, const hgp_param
   hgp_status st = HGP_OK;
   const uint32_t nn = nb->hi - nb->lo;
   uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
-  uint32_t *lists = scratch_raw<uint32_t>(c, 3 * (size_t)(nn ? nn : 1), &st);
+  uint32_t *lists = scratch_raw<uint32_t>(c, 4 * (size_t)(nn ? nn : 1), &st);
   if (st) return st;
   J.nb_off = nb->off; J.nbr = nb->nbr; J.cand = cand;
   if (nn) {
@@ -383,7 +428,7 @@ hgp_status score_list_segments(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max
                                const uint32_t *list_count) {
   hgp_status st = HGP_OK;
   uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
-  uint32_t *lists = scratch_raw<uint32_t>(c, 3 * (size_t)(nn ? nn : 1), &st);
+  uint32_t *lists = scratch_raw<uint32_t>(c, 4 * (size_t)(nn ? nn : 1), &st);
   if (st) return st;
   if (J.pi <= 4) return launch_score_tiers<4>(c, J, nn, max_deg, lists, counts, list, list_count);
   return launch_score_tiers<16>(c, J, nn, max_deg, lists, counts, list, list_count);

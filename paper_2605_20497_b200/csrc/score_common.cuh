@@ -31,7 +31,7 @@ struct ScoreJob {
   uint32_t *wide_list, *wide_count;  // deferred: packed 32-bit accumulator would overflow
 };
 
-enum { kModeP32 = 0, kModeWide = 1 };
+enum { kModeP32 = 0, kModeWide = 1, kModeSplit = 2 };
 
 template <int PIMAX>
 struct Top {   // best-first list of (score, id); empty entries are (0, 0): every real score >= 1
