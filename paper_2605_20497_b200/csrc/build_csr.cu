@@ -170,8 +170,10 @@ struct IncBlockSeg {   // segment 2n = in(n), 2n+1 = out(n)
 // Given edge_off/edge_nsrc/pins/edge_mu of g (device), allocate and fill inc_off, inc_nin,
 // inc, in_mu and g->max_inc. Synchronises (reads max degree).
 hgp_status build_incidence(hgp_ctx *c, hgp_csr *g) {
-  static const bool atomic_path = getenv("HGP_INC_ATOMIC") != nullptr;   // A/B switch (measurement)
-  if (!atomic_path && g->P < (1ull << 30) && g->N < (1u << 30)) return build_incidence_radix(c, g);
+  // The radix transpose (radix.cu) is exact and deterministic but measured slower on B200 at C2
+  // (a1 9.5 vs 7.4 ms: its first scatter pass runs at ~0.5 TB/s); opt in with HGP_INC_RADIX=1.
+  const bool radix_path = getenv("HGP_INC_RADIX") != nullptr;
+  if (radix_path && g->P < (1ull << 30) && g->N < (1u << 30)) return build_incidence_radix(c, g);
   hgp_status st = HGP_OK;
   const uint32_t N = g->N, E = g->E;
   const uint64_t P = g->P;

@@ -63,6 +63,8 @@ __device__ __forceinline__ void eval_top(const ScoreJob &J, const FusedJob &F, u
     const bool ok = wn + J.node_w[v] <= J.omega && (J.delta == HGP_UNBOUNDED || uni <= J.delta);
     F.pool[base + i] = ok ? v : (v | kPurge);
     if (!ok) continue;
+    // packed keys: even the largest noise cannot lift (score, id) above the current pi-th best
+    if (PACKED && ((((e_nm + J.noise_cap) << 32) | v) <= thr)) continue;
     uint64_t sc = e_nm;
     if (J.noise_cap) {
       const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
@@ -273,13 +275,15 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       uint4 ra = rowA[k];
       uint2 rb = rowB[k];
       bool full = false;
-      for (uint32_t f0 = flo; f0 < fhi; f0 += 128) {
+      // one 128-pin window of this warp's range; FULL: the window lies inside [flo, fhi)
+      auto window = [&](uint32_t f0, auto full_tag) {
+        constexpr bool FULL = decltype(full_tag)::value;
         uint32_t m[4], add[4], sl[4], kk[4];
         bool val[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t f = f0 + u * 32 + lane;
-          val[u] = f < fhi;
+          val[u] = FULL || f < fhi;
           if (val[u]) {
             while (f >= rb.x) { ++k; ra = rowA[k]; rb = rowB[k]; }   // next incident edge
           }
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
           val[u] = miss != 0;                                      // val now marks the misses
           any_miss |= miss;
         }
-        if (__any_sync(0xFFFFFFFFu, any_miss != 0)) {                   // displaced keys: probe on
+        if (__any_sync(0xFFFFFFFFu, any_miss != 0)) {              // displaced keys: probe on
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (!val[u]) continue;
@@ -334,7 +338,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
             if (!full) red_add_u32(acc_s + 4 * slot, add[u]);
           }
         }
-      }
+      };
+      uint32_t f0 = flo;
+      for (; f0 + 128 <= fhi; f0 += 128) window(f0, std::true_type{});
+      if (f0 < fhi) window(f0, std::false_type{});
       if (full) s_full = 1;
       __syncthreads();                                             // rows are rewritten by the next tile
       if (s_full) break;

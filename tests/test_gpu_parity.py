@@ -315,3 +315,23 @@ def test_fused_level0_partial_paths(hgp, ctx, monkeypatch, mode, name, make, ome
         assert np.array_equal(gam.cpu().numpy(), rr["gamma"])
         assert_csr_equal(cg.to_host(), rr["coarse"], f"{mode} coarse")
         assert_nbrs_equal(cnb.to_host(), rr["coarse_nb"], f"{mode} coarse nbrs")
+
+
+@pytest.mark.parametrize("name,make", [("C1", lambda: hgpgen.tiny(1)), ("tiny-N", lambda: hgpgen.tiny(3, num_nodes=100, num_edges=200)),
+                                       ("vlsi-small", lambda: hgpgen.vlsi(6, 20000, 20000, dmax=1024, in_cap=600)),
+                                       ("snn-small", lambda: hgpgen.snn(5, layers=4, rows=20, cols=20, fanout=30,
+                                                                         window=9, rewire=0.1))])
+def test_radix_incidence_matches_oracle(hgp, ctx, monkeypatch, name, make):
+    """a1 with the radix-sort transpose (HGP_INC_RADIX=1; 1, 2 or 3 passes by node count) builds the
+    same canonical incidence as the oracle, and so does a5's coarse incidence."""
+    monkeypatch.setenv("HGP_INC_RADIX", "1")
+    hg = make()
+    g = gpu_build(hgp, ctx, hg)
+    rg = ref.build_csr_hg(hg)
+    assert_csr_equal(g.to_host(), rg, "a1 (radix)")
+    nb = hgp.unique_neighbors(ctx, g)
+    m = torch.empty(g.N, dtype=torch.uint32, device="cuda")
+    gam = torch.empty(g.N, dtype=torch.uint32, device="cuda")
+    cg, cnb, _ = hgp.coarsen_level(ctx, g, nb, hgp.params(64, 600, 4), None, m, gam)
+    rr = ref.coarsen_level(rg, ref.unique_neighbors(rg), ref.params(64, 600, 4))
+    assert_csr_equal(cg.to_host(), rr["coarse"], "a5 (radix)")
