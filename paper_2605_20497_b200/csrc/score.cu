@@ -316,26 +316,19 @@ hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_
     attr = true;
   }
   uint32_t *bigA = lists, *wide = lists + nn, *huge = lists + 2 * (size_t)nn;
-  // A: every node; larger neighbourhoods -> bigA, packed overflow -> wide
-  J.list = first_list; J.list_count = first_count; J.cap = 1u << (kSALog - 1); J.log2s = kSALog;
+  // F (score_flat.cu): every node with |N(n)| <= 2048, packed or split accumulators; larger
+  // neighbourhoods -> bigA, nodes needing 64-bit eta -> wide
+  J.list = first_list; J.list_count = first_count;
   J.big_list = bigA; J.big_count = counts + 0; J.wide_list = wide; J.wide_count = counts + 1;
-  const uint32_t gA = first_list ? 8u * c->sm_count : (nn < 64u * c->sm_count ? nn : 64u * c->sm_count);
-  HGP_TRY(launch(c, "score_A", k_score<kSAThreads, kModeP32, true, PIMAX>, dim3(gA), dim3(kSAThreads), (8u << kSALog) + 16,
-                 J));
-  if (max_deg > (1u << (kSALog - 1))) {   // B: big neighbourhoods, packed
+  HGP_TRY(launch_score_flat<PIMAX>(c, J, nn, J.E));
+  if (max_deg > (1u << (kSALog - 1))) {   // B: big neighbourhoods, packed (overflow -> wide)
     J.list = bigA; J.list_count = counts + 0; J.cap = 1u << (kSBLog - 1); J.log2s = kSBLog;
     J.big_list = huge; J.big_count = counts + 2;
     HGP_TRY(launch(c, "score_B", k_score<kSBThreads, kModeP32, true, PIMAX>, dim3(c->sm_count), dim3(kSBThreads),
                    (8u << kSBLog) + 16, J));
   }
-  // S: nodes whose packed sums could overflow 32 bits but whose eta fits u32 (split accumulators)
-  uint32_t *wide2 = lists + 3 * (size_t)nn;
-  J.list = wide; J.list_count = counts + 1; J.cap = 1u << (kSSLog - 1); J.log2s = kSSLog;
-  J.big_list = huge; J.big_count = counts + 2; J.wide_list = wide2; J.wide_count = counts + 3;
-  HGP_TRY(launch(c, "score_S", k_score<kSSThreads, kModeSplit, true, PIMAX>, dim3(4 * c->sm_count), dim3(kSSThreads),
-                 (12u << kSSLog) + 32, J));
   // W: the rest (neighbourhoods up to 2048)
-  J.list = wide2; J.list_count = counts + 3; J.cap = 1u << (kSWLog - 1); J.log2s = kSWLog;
+  J.list = wide; J.list_count = counts + 1; J.cap = 1u << (kSWLog - 1); J.log2s = kSWLog;
   J.big_list = huge; J.big_count = counts + 2;
   HGP_TRY(launch(c, "score_W", k_score<kSWThreads, kModeWide, true, PIMAX>, dim3(c->sm_count), dim3(kSWThreads),
                  16u << kSWLog, J));
@@ -392,6 +385,7 @@ hgp_status score_prologue(hgp_ctx *c, const hgp_csr *g, uint32_t lo, uint32_t hi
   J->omega = p->omega; J->delta = p->delta; J->noise_cap = p->noise_cap;
   J->seed_mix = splitmix64_host(p->noise_seed);
   J->pi = p->pi; J->norm = p->norm;
+  J->E = g->E;
   return HGP_OK;
 }
 

@@ -20,6 +20,7 @@ struct ScoreJob {
   // params
   uint64_t omega, delta, noise_cap, seed_mix;
   uint32_t pi, norm;
+  uint32_t E;                  // edges of the level (per-edge c(e) precompute)
   hgp_cand *cand;
   // scheduling
   const uint32_t *list;        // nodes of this launch (nullptr: every node of [lo,hi))
@@ -32,6 +33,9 @@ struct ScoreJob {
 };
 
 enum { kModeP32 = 0, kModeWide = 1, kModeSplit = 2 };
+
+template <int PIMAX>
+hgp_status launch_score_flat(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t E);
 
 template <int PIMAX>
 struct Top {   // best-first list of (score, id); empty entries are (0, 0): every real score >= 1
