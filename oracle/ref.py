@@ -233,13 +233,57 @@ def contract(g: Csr, nb: Nbrs, match_arr: np.ndarray):
     return gamma, _take_csr(oc), _take_nbrs(on)
 
 
-def coarsen_level(g: Csr, nb: Nbrs, p: CParams):
-    """score -> match -> contract; nb flags are written in place. Returns a dict."""
+def coarsen_level(g: Csr, nb: Nbrs, p: CParams, leftover: bool = False):
+    """score -> match (-> f2 leftover pairing if asked) -> contract; nb flags are written in place.
+    Returns a dict."""
     cand = score_pairs(g, nb, p)
     m, per, val = match(cand, p.pi)
+    if leftover:
+        m, extra = leftover_pairs(cand, g.node_w, g.in_mu, p.omega, p.delta, m)
     gamma, cg, cnb = contract(g, nb, m)
     return {"cand": cand, "match": m, "matched_per_round": per, "round_value": val,
             "gamma": gamma, "coarse": cg, "coarse_nb": cnb}
+
+
+def leftover_targets(cand: np.ndarray, node_w: np.ndarray, in_mu: np.ndarray, omega: int, delta: int) -> np.ndarray:
+    """SURVEY §8(f) f2, the best-effort pairing of P:673-677 read deterministically (DESIGN
+    reading #22). L = the nodes left with no candidate (cand[n][0] = NONE; they have no valid
+    neighbour, so a4 never matches them). Each n in L targets, among m in L \ {n} with
+    size(n) + size(m) <= Omega and in_mu(n) + in_mu(m) <= Delta (the paper's over-estimate of
+    the inbound union), the one with the largest (size(m), m) — "sorted by size ... the
+    first valid node it finds", contentions broken by id. Score = size(n) + size(m). Returns a
+    [N, 1] candidate array (NONE outside L / without a valid partner). Plain O(|L|^2) loops."""
+    N = cand.shape[0]
+    out = np.zeros((N, 1), dtype=CAND_DTYPE)
+    out["id"] = NONE
+    L = [n for n in range(N) if int(cand[n][0]["id"]) == NONE]
+    w = [int(x) for x in node_w]
+    im = [int(x) for x in in_mu]
+    for n in L:
+        best = None
+        for m in L:
+            if m == n or w[n] + w[m] > omega:
+                continue
+            if delta != UNBOUNDED and im[n] + im[m] > delta:
+                continue
+            if best is None or (w[m], m) > (w[best], best):
+                best = m
+        if best is not None:
+            out[n, 0] = (best, 0, w[n] + w[best])
+    return out
+
+
+def leftover_pairs(cand: np.ndarray, node_w: np.ndarray, in_mu: np.ndarray, omega: int, delta: int,
+                   match_arr: np.ndarray):
+    """f2: the targets of leftover_targets solved by the a4 DP as one extra round (pi = 1) and
+    merged into match_arr. Returns (match [N], pairs added)."""
+    c2 = leftover_targets(cand, node_w, in_mu, omega, delta)
+    m2, per2, _ = match(c2, 1)
+    out = np.array(match_arr, dtype=np.uint32, copy=True)
+    sel = m2 != NONE
+    assert np.all(out[sel] == NONE), "a leftover node was already matched"
+    out[sel] = m2[sel]
+    return out, int(per2[0])
 
 
 def stop_nodes(g0: Csr, omega: int) -> int:
