@@ -54,6 +54,7 @@ extern "C" {
 #define HGP_PURGE 0x80000000u             /* neighbour entry flag: permanently invalid */
 #define HGP_MAX_PI 16
 #define HGP_MAX_LEVELS 64   /* hgp_coarsen: at most this many levels */
+#define HGP_FLAG_LEFTOVER 1u /* hgp_params.flags: run hgp_leftover_pairs after a4 */
 
 typedef enum {
   HGP_OK = 0,
@@ -130,7 +131,7 @@ typedef struct {
   uint64_t noise_seed;        /* deterministic symmetric noise */
   uint64_t noise_cap;         /* noise in [0, cap], 2^-24 units; 0 disables; cap < 2^56 */
   uint32_t batch;             /* tuning only; results never depend on it */
-  uint32_t flags;             /* reserved, 0 */
+  uint32_t flags;             /* HGP_FLAG_* bits; 0 = the level exactly as §8(a) defines it */
 } hgp_params;
 
 typedef struct {
@@ -213,6 +214,17 @@ HGP_API hgp_status hgp_shard_bounds(hgp_ctx *ctx, const hgp_csr *g, uint32_t wor
 HGP_API hgp_status hgp_coarsen_level0(hgp_ctx *ctx, const hgp_csr *g, const hgp_params *p, hgp_cand *cand,
                                       uint32_t *match, uint32_t *gamma, hgp_nbrs *nb, hgp_csr *coarse,
                                       hgp_nbrs *coarse_nb, hgp_level_stats *stats);
+
+/* f2 (DESIGN reading #22): deterministic best-effort pairing of the
+ * nodes left without any candidate (cand[n][0].id == HGP_NONE; a4 never matches them). Each such n
+ * targets the other such m with the largest (node_w[m], m) satisfying node_w[n] + node_w[m] <= omega
+ * and in_mu[n] + in_mu[m] <= delta (the paper's over-estimate of the inbound union); score
+ * node_w[n] + node_w[m]; the resulting two-cycle pseudo-forest is solved by the a4 DP as one round
+ * and merged into match (DEVICE [N], in/out). cand: DEVICE [N][pi] from a3; node_w, in_mu: DEVICE
+ * [N] of the level; added: DEVICE [1] pairs added, or NULL. Synchronises (scan totals). */
+HGP_API hgp_status hgp_leftover_pairs(hgp_ctx *ctx, const hgp_cand *cand, uint32_t N, uint32_t pi,
+                                      const uint32_t *node_w, const uint32_t *in_mu, uint64_t omega,
+                                      uint64_t delta, uint32_t *match, uint32_t *added);
 
 /* Multi-level coarsening driver (paper §5): level 0 by
  * hgp_coarsen_level0, level l >= 1 by hgp_coarsen_level on the previous coarse CSR and coarse

@@ -248,7 +248,7 @@ def coarsen_level(g: Csr, nb: Nbrs, p: CParams, leftover: bool = False):
 def leftover_targets(cand: np.ndarray, node_w: np.ndarray, in_mu: np.ndarray, omega: int, delta: int) -> np.ndarray:
     """SURVEY §8(f) f2, the best-effort pairing of P:673-677 read deterministically (DESIGN
     reading #22). L = the nodes left with no candidate (cand[n][0] = NONE; they have no valid
-    neighbour, so a4 never matches them). Each n in L targets, among m in L \ {n} with
+    neighbour, so a4 never matches them). Each n in L targets, among the other m in L with
     size(n) + size(m) <= Omega and in_mu(n) + in_mu(m) <= Delta (the paper's over-estimate of
     the inbound union), the one with the largest (size(m), m) — "sorted by size ... the
     first valid node it finds", contentions broken by id. Score = size(n) + size(m). Returns a
@@ -293,7 +293,7 @@ def stop_nodes(g0: Csr, omega: int) -> int:
     return 1 if omega == UNBOUNDED else max(1, -(-W // int(omega)))
 
 
-def coarsen(g0: Csr, p: CParams, max_levels: int = 64) -> dict:
+def coarsen(g0: Csr, p: CParams, max_levels: int = 64, leftover: bool = False) -> dict:
     """Multi-level driver, written out plainly: level l is
     coarsen_level on the previous level's coarse CSR and neighbour lists, with noise seed
     p.noise_seed + l (reading #3: "the driver passes seed+level"); it stops after the first level
@@ -306,7 +306,7 @@ def coarsen(g0: Csr, p: CParams, max_levels: int = 64) -> dict:
     levels = []
     for lvl in range(max_levels):
         pl = params(p.omega, p.delta, p.pi, norm=p.norm, noise_seed=p.noise_seed + lvl, noise_cap=p.noise_cap)
-        r = coarsen_level(g, nb, pl)
+        r = coarsen_level(g, nb, pl, leftover)
         rho = r["gamma"][rho]
         per = [int(x) for x in r["matched_per_round"]]
         cg = r["coarse"]

@@ -7,6 +7,12 @@ namespace hgp {
 hgp_status build_incidence(hgp_ctx *c, hgp_csr *g);
 // The same by a stable LSD radix sort of (pin << 1 | is_src, edge) pairs (radix.cu); P < 2^30.
 hgp_status build_incidence_radix(hgp_ctx *c, hgp_csr *g);
+// Stable LSD radix sort of (key, value) u32 pairs by key < 2^kbits (radix.cu); n < 2^30.
+hgp_status radix_sort_pairs(hgp_ctx *c, uint32_t *keys, uint32_t *vals, uint32_t *keys_alt, uint32_t *vals_alt,
+                            uint64_t n, uint32_t kbits, uint32_t **ko, uint32_t **vo);
+// f2 leftover pairing (leftover.cu): extends match in place.
+hgp_status leftover_impl(hgp_ctx *c, const hgp_cand *cand, uint32_t N, uint32_t pi, const uint32_t *node_w,
+                         const uint32_t *in_mu, uint64_t omega, uint64_t delta, uint32_t *match, uint32_t *added);
 void free_csr(hgp_ctx *c, hgp_csr *g);
 void free_nbrs(hgp_ctx *c, hgp_nbrs *nb);
 // Neighbour segments left in the fused kernel's pool (not compacted into a CSR): segment n is

@@ -24,6 +24,8 @@ extern "C" hgp_status hgp_coarsen_level(hgp_ctx *c, const hgp_csr *g, hgp_nbrs *
   HGP_TRY(hgp_score_pairs(c, g, nb, p, cand));
   HGP_CUDA(cudaEventRecord(c->ev[1], c->stream));
   HGP_TRY(hgp_match(c, cand, g->N, p->pi, match, per));
+  if (p->flags & HGP_FLAG_LEFTOVER)
+    HGP_TRY(leftover_impl(c, cand, g->N, p->pi, g->node_w, g->in_mu, p->omega, p->delta, match, nullptr));
   HGP_CUDA(cudaEventRecord(c->ev[2], c->stream));
   hgp_status s = contract_impl(c, g, nb, match, gamma, coarse, coarse_nb, stats, nullptr);
   if (s != HGP_OK) { free_csr(c, coarse); free_nbrs(c, coarse_nb); return s; }

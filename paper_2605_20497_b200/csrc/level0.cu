@@ -710,6 +710,8 @@ extern "C" hgp_status hgp_coarsen_level0(hgp_ctx *c, const hgp_csr *g, const hgp
   HGP_CUDA(cudaEventRecord(c->ev[1], c->stream));
   auto cleanup = [&]() { if (!have_view && !nb) free_nbrs(c, &local); };
   hgp_status s = hgp_match(c, cand, g->N, p->pi, match, per);
+  if (s == HGP_OK && (p->flags & HGP_FLAG_LEFTOVER))
+    s = leftover_impl(c, cand, g->N, p->pi, g->node_w, g->in_mu, p->omega, p->delta, match, nullptr);
   if (s != HGP_OK) { cleanup(); if (nb) free_nbrs(c, nb); return s; }
   HGP_CUDA(cudaEventRecord(c->ev[2], c->stream));
   s = contract_impl(c, g, have_view ? nullptr : use, match, gamma, coarse, coarse_nb, stats, have_view ? &view : nullptr);

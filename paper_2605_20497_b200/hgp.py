@@ -121,6 +121,9 @@ def lib():
         L.hgp_coarsen.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.POINTER(CParams), ctypes.c_uint32, vp,
                                   ctypes.POINTER(CCsr), ctypes.POINTER(CNbrs), vp, ctypes.POINTER(ctypes.c_uint32)]
         L.hgp_coarsen.restype = S
+        L.hgp_leftover_pairs.argtypes = [vp, vp, ctypes.c_uint32, ctypes.c_uint32, vp, vp, ctypes.c_uint64,
+                                         ctypes.c_uint64, vp, vp]
+        L.hgp_leftover_pairs.restype = S
         L.hgp_neighbors_and_scores.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.POINTER(CParams), ctypes.c_uint32,
                                                ctypes.c_uint32, ctypes.POINTER(CNbrs), vp]
         L.hgp_shard_bounds.argtypes = [vp, ctypes.POINTER(CCsr), ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32)]
@@ -238,9 +241,12 @@ class Ctx:
         _check(lib().hgp_copy(self.h, vp(dst_ptr), vp(src_ptr), nbytes))
 
 
+FLAG_LEFTOVER = 1   # hgp_params.flags: f2 leftover pairing after a4
+
+
 def params(omega: int, delta: int, pi: int = 4, norm: int = 0, noise_seed: int = 0, noise_cap: int = 0,
-           batch: int = 0) -> CParams:
-    return CParams(omega, delta, pi, norm, noise_seed, noise_cap, batch, 0)
+           batch: int = 0, flags: int = 0) -> CParams:
+    return CParams(omega, delta, pi, norm, noise_seed, noise_cap, batch, flags)
 
 
 class Csr:
@@ -385,6 +391,16 @@ def coarsen_level0(ctx: Ctx, g: Csr, p: CParams, cand: torch.Tensor | None, matc
 
 
 MAX_LEVELS = 64
+
+
+def leftover_pairs(ctx: Ctx, cand: torch.Tensor, N: int, pi: int, node_w: torch.Tensor, in_mu: torch.Tensor,
+                   omega: int, delta: int, match_t: torch.Tensor) -> int:
+    """f2 (hgp_leftover_pairs): pairs the nodes left without candidates; extends match_t in place.
+    Returns the number of pairs added."""
+    added = torch.zeros(1, dtype=torch.uint32, device="cuda")
+    _check(lib().hgp_leftover_pairs(ctx.h, _ptr(cand), N, pi, _ptr(node_w), _ptr(in_mu), omega, delta,
+                                    _ptr(match_t), _ptr(added)))
+    return int(added.item())
 
 
 def coarsen(ctx: Ctx, g: Csr, p: CParams, max_levels: int = MAX_LEVELS):
