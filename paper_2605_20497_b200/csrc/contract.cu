@@ -351,14 +351,16 @@ struct BoundIn {   // |N(a)| + |N(b)| per coarse node
   }
 };
 
-__global__ void k_cnbr_classify(const uint64_t *bound_off, uint32_t Nc, uint32_t capA, uint32_t capB, uint32_t *listB,
-                                uint32_t *listC, uint32_t *counts, unsigned long long *maxb) {
+__global__ void k_cnbr_classify(const uint64_t *bound_off, uint32_t Nc, uint32_t capA, uint32_t capM, uint32_t capB,
+                                uint32_t *listM, uint32_t *listB, uint32_t *listC, uint32_t *counts,
+                                unsigned long long *maxb) {
   uint64_t mx = 0;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < Nc; c += gridDim.x * blockDim.x) {
     const uint64_t d = bound_off[c + 1] - bound_off[c];
     if (d > capA) {
-      if (d <= capB) listB[atomicAdd(&counts[0], 1u)] = c;
-      else { listC[atomicAdd(&counts[1], 1u)] = c; mx = d > mx ? d : mx; }
+      if (d <= capM) listM[atomicAdd(&counts[0], 1u)] = c;
+      else if (d <= capB) listB[atomicAdd(&counts[1], 1u)] = c;
+      else { listC[atomicAdd(&counts[2], 1u)] = c; mx = d > mx ? d : mx; }
     }
   }
   mx = warp_max(mx);
@@ -388,6 +390,7 @@ __global__ void k_count_kept(const uint32_t *rep, uint32_t E, uint32_t *out) {
 }
 
 static constexpr uint32_t kCALog = 12, kCAThreads = 256;   // 4096 slots: 16 KB, <= 2048 entries
+static constexpr uint32_t kCMLog = 14, kCMThreads = 256;   // 16384 slots: 64 KB, <= 8192 entries (3 CTAs/SM)
 static constexpr uint32_t kCBLog = 15, kCBThreads = 256;   // 32768 slots: 128 KB, <= 16384 entries
 
 hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match, uint32_t *gamma,
@@ -488,13 +491,15 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   HGP_TRY(scan_exclusive(c, BoundIn{mem0, mem1, seg_off, view ? view->len : nullptr}, Nc, bound_off, &Vb));
   uint32_t *pool = scratch_raw<uint32_t>(c, Vb, &st);
   uint32_t *ccnt = scratch_raw<uint32_t>(c, Nc, &st);
-  uint32_t *lists = scratch_raw<uint32_t>(c, 2 * (size_t)Nc, &st);
+  uint32_t *lists = scratch_raw<uint32_t>(c, 3 * (size_t)Nc, &st);
   uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
   unsigned long long *misc = scratch_zero<unsigned long long>(c, 2, &st);   // purged, max bound (tier C)
   if (st) return st;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_coarse_nbrs<kCAThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kCALog);
+    // tiers M and B share the instantiation <256, true>: the attribute is the larger table's
+    static_assert(kCMThreads == kCBThreads && kCMLog < kCBLog, "M and B share one instantiation");
     cudaFuncSetAttribute(k_coarse_nbrs<kCBThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kCBLog);
     attr = true;
   }
@@ -503,28 +508,33 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   J.nb_start = view ? view->start : nullptr; J.nb_len = view ? view->len : nullptr;
   J.nbr = view ? view->nbr : nb->nbr;
   J.pool = pool; J.cnt = ccnt; J.Nc = Nc; J.purged = misc;
-  const uint32_t capA = 1u << (kCALog - 1), capB = 1u << (kCBLog - 1);
+  const uint32_t capA = 1u << (kCALog - 1), capM = 1u << (kCMLog - 1), capB = 1u << (kCBLog - 1);
   J.list = nullptr; J.list_count = nullptr; J.cap = capA; J.log2s = kCALog;
   const uint32_t gA = Nc < 64u * c->sm_count ? (Nc ? Nc : 1) : 64u * c->sm_count;
   HGP_TRY(launch(c, "coarse_nbrs_A", k_coarse_nbrs<kCAThreads, true>, dim3(gA), dim3(kCAThreads), 4u << kCALog, J));
   HGP_TRY(launch(c, "cnbr_classify", k_cnbr_classify, dim3(grid_for(Nc)), dim3(256), 0, (const uint64_t *)bound_off, Nc,
-                 capA, capB, lists, lists + Nc, counts, misc + 1));
-  uint32_t hc[2];
-  HGP_TRY(read_back(c, counts, 8, hc));
+                 capA, capM, capB, lists, lists + Nc, lists + 2 * (size_t)Nc, counts, misc + 1));
+  uint32_t hc[3];
+  HGP_TRY(read_back(c, counts, 12, hc));
   if (hc[0]) {
-    J.list = lists; J.list_count = counts; J.cap = capB; J.log2s = kCBLog;
+    J.list = lists; J.list_count = counts; J.cap = capM; J.log2s = kCMLog;
+    HGP_TRY(launch(c, "coarse_nbrs_M", k_coarse_nbrs<kCMThreads, true>, dim3(3 * c->sm_count), dim3(kCMThreads),
+                   4u << kCMLog, J));
+  }
+  if (hc[1]) {
+    J.list = lists + Nc; J.list_count = counts + 1; J.cap = capB; J.log2s = kCBLog;
     HGP_TRY(launch(c, "coarse_nbrs_B", k_coarse_nbrs<kCBThreads, true>, dim3(c->sm_count), dim3(kCBThreads),
                    4u << kCBLog, J));
   }
-  if (hc[1]) {
+  if (hc[2]) {
     uint64_t mb = 0;
     HGP_TRY(read_u64(c, (const uint64_t *)(misc + 1), &mb));
     uint32_t lg = kCBLog;
     while ((1ull << (lg - 1)) < mb) ++lg;
-    const uint32_t ctas = hc[1] < (uint32_t)c->sm_count ? hc[1] : (uint32_t)c->sm_count;
+    const uint32_t ctas = hc[2] < (uint32_t)c->sm_count ? hc[2] : (uint32_t)c->sm_count;
     uint32_t *gtab = scratch_raw<uint32_t>(c, (size_t)ctas << lg, &st);
     if (st) return st;
-    J.list = lists + Nc; J.list_count = counts + 1; J.cap = 0xFFFFFFFFu; J.log2s = lg; J.gtab = gtab;
+    J.list = lists + 2 * (size_t)Nc; J.list_count = counts + 2; J.cap = 0xFFFFFFFFu; J.log2s = lg; J.gtab = gtab;
     HGP_TRY(launch(c, "coarse_nbrs_C", k_coarse_nbrs<256, false>, dim3(ctas), dim3(256), 0, J));
   }
   CN->lo = 0;

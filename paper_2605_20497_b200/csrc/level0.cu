@@ -35,6 +35,7 @@ struct FusedJob {
   uint32_t *pool_list, *pool_count;       // pool full (cnt[n] holds the exact count) -> second pool
   uint64_t start_bias;                    // added to every start written
   const uint64_t *cv;                     // [E] c(e), Eq.5 term in 2^-24 fixed point
+  const uint2 *wmu;                       // [N] (size, in_mu) packed for the validity test
 };
 
 // Phase 2b + 3 of k_nbrscore. PACKED: every score of the node is < 2^32, so (score, id) is
@@ -59,8 +60,9 @@ __device__ __forceinline__ void eval_top(const ScoreJob &J, const FusedJob &F, u
     const uint32_t x = acc[slot];
     const uint64_t e_nm = (uint64_t)(ib < 32 ? x >> ib : 0) * g;
     const uint64_t inter = x & imask;
-    const uint64_t uni = (uint64_t)inn + J.in_mu[v] - inter;      // |in(n) ∪ in(m)|
-    const bool ok = wn + J.node_w[v] <= J.omega && (J.delta == HGP_UNBOUNDED || uni <= J.delta);
+    const uint2 wm = __ldg(F.wmu + v);                             // (size(m), in_mu(m)): one gather
+    const uint64_t uni = (uint64_t)inn + wm.y - inter;             // |in(n) ∪ in(m)|
+    const bool ok = wn + wm.x <= J.omega && (J.delta == HGP_UNBOUNDED || uni <= J.delta);
     F.pool[base + i] = ok ? v : (v | kPurge);
     if (!ok) continue;
     // packed keys: even the largest noise cannot lift (score, id) above the current pi-th best
@@ -427,6 +429,11 @@ __global__ void k_fused_pack(const uint32_t *pool, const uint64_t *start, const 
   if (lane == 0) atomicMax(maxdeg, mx);
 }
 
+__global__ void k_pack_wmu(const uint32_t *node_w, const uint32_t *in_mu, uint32_t N, uint2 *wmu) {
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
+    wmu[n] = make_uint2(node_w[n], in_mu[n]);
+}
+
 __global__ void k_edge_cv(const uint64_t *edge_off, const uint32_t *edge_w, uint32_t E, uint32_t norm, uint64_t *cv) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
     const uint64_t we = (uint64_t)edge_w[e] << HGP_FP_SHIFT;   // Eq.5 term c(e), 2^-24 fixed point
@@ -442,6 +449,19 @@ __global__ void k_pairs_total(const uint64_t *edge_off, uint32_t E, unsigned lon
   }
   s = warp_sum(s);
   if (lane_id() == 0) atomicAdd(T, (unsigned long long)s);
+}
+
+__global__ void k_sample_lists(uint32_t lo, uint32_t nn, uint32_t stride, uint32_t *sample, uint32_t *rest,
+                               uint32_t *counts) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
+    const uint32_t q = i / stride;
+    if (i % stride == 0) sample[q] = lo + i;
+    else rest[i - q - 1] = lo + i;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    counts[0] = (nn + stride - 1) / stride;
+    counts[1] = nn - counts[0];
+  }
 }
 
 // tiers of the fused kernel: A 4096 slots (40 KB incl. the dense list) for every node, M 8192
@@ -470,12 +490,42 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
     attr = true;
   }
   const uint32_t sm = c->sm_count;
-  F.list = L.in_list; F.list_count = L.in_count; F.log2s = kFALog;
-  F.defer_list = L.la; F.defer_count = L.ca;
   const uint32_t per_sm = MINB;                                     // exactly the resident CTAs
   const uint32_t gA = L.hn < per_sm * sm ? L.hn : per_sm * sm;
   if (gA == 0) return HGP_OK;
-  HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
+  constexpr uint32_t kStride = 64;
+  const char *smin = getenv("HGP_FUSED_SAMPLE_MIN");                // test hook: sample small levels too
+  const uint32_t sample_min = smin ? (uint32_t)strtoul(smin, nullptr, 10) : 1024 * kStride;
+  if (!L.in_list && L.hn >= sample_min && L.hn >= 2 * kStride) {
+    // Tier A on every 64th node first: if most of them overflow its table (large neighbourhoods,
+    // e.g. the rewired SNN), the other nodes start in tier M instead of paying a wasted traversal
+    // in A. Results do not depend on the choice (every tier computes the same exact values).
+    hgp_status st = HGP_OK;
+    uint32_t *sample = scratch_raw<uint32_t>(c, L.hn / kStride + 1, &st);
+    uint32_t *rest = scratch_raw<uint32_t>(c, L.hn, &st);
+    uint32_t *cnt2 = scratch_zero<uint32_t>(c, 2, &st);
+    if (st) return st;
+    HGP_TRY(launch(c, "sample_lists", k_sample_lists, dim3(div_up(L.hn, 256) < 4096 ? div_up(L.hn, 256) : 4096), dim3(256),
+                   0, F.S.lo, L.hn, kStride, sample, rest, cnt2));
+    F.list = sample; F.list_count = cnt2; F.log2s = kFALog;
+    F.defer_list = L.la; F.defer_count = L.ca;
+    HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
+    uint32_t deferred = 0;
+    HGP_TRY(read_back(c, L.ca, 4, &deferred));
+    const uint32_t ns = (L.hn + kStride - 1) / kStride;
+    F.list = rest; F.list_count = cnt2 + 1;
+    if (4 * deferred > ns) {                                        // > 25 %: start in M
+      F.log2s = kFMLog; F.defer_list = L.lm; F.defer_count = L.cm;
+      HGP_TRY(launch(c, "nbrscore_M", k_nbrscore<kFMThreads, PIMAX, 3, kFMLog>, dim3(3 * sm), dim3(kFMThreads),
+                     fused_smem(kFMLog), F));
+    } else {
+      HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
+    }
+  } else {
+    F.list = L.in_list; F.list_count = L.in_count; F.log2s = kFALog;
+    F.defer_list = L.la; F.defer_count = L.ca;
+    HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
+  }
   F.list = L.la; F.list_count = L.ca; F.log2s = kFMLog;
   F.defer_list = L.lm; F.defer_count = L.cm;
   HGP_TRY(launch(c, "nbrscore_M", k_nbrscore<kFMThreads, PIMAX, 3, kFMLog>, dim3(3 * sm), dim3(kFMThreads), fused_smem(kFMLog), F));
@@ -550,9 +600,14 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   if (st) return st;
   HGP_TRY(launch(c, "edge_cv", k_edge_cv, dim3(g->E ? (div_up(g->E, 256) < 4096 ? div_up(g->E, 256) : 4096) : 0), dim3(256), 0,
                  (const uint64_t *)g->edge_off, (const uint32_t *)g->edge_w, g->E, p->norm, cv));
+  uint2 *wmu = scratch_raw<uint2>(c, g->N ? g->N : 1, &st);
+  if (st) return st;
+  HGP_TRY(launch(c, "pack_wmu", k_pack_wmu, dim3(g->N ? (div_up(g->N, 256) < 4096 ? div_up(g->N, 256) : 4096) : 0),
+                 dim3(256), 0, (const uint32_t *)g->node_w, (const uint32_t *)g->in_mu, g->N, wmu));
   FusedJob F{};
   F.S = J;
   F.cv = cv;
+  F.wmu = wmu;
   F.pool = pool; F.pool_cap = pool_cap; F.pool_cursor = misc + 1; F.start = start; F.cnt = cnt;
   F.pool_list = LP; F.pool_count = counts + 3;
   TierLists L{nullptr, nullptr, nn, LA, counts + 0, LM, counts + 1, LD, counts + 2};

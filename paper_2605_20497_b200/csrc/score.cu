@@ -386,6 +386,7 @@ hgp_status score_prologue(hgp_ctx *c, const hgp_csr *g, uint32_t lo, uint32_t hi
   J->seed_mix = splitmix64_host(p->noise_seed);
   J->pi = p->pi; J->norm = p->norm;
   J->E = g->E;
+  J->N = g->N;
   return HGP_OK;
 }
 

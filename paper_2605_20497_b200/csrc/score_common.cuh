@@ -20,7 +20,7 @@ struct ScoreJob {
   // params
   uint64_t omega, delta, noise_cap, seed_mix;
   uint32_t pi, norm;
-  uint32_t E;                  // edges of the level (per-edge c(e) precompute)
+  uint32_t E, N;               // edges / nodes of the level (per-edge and per-node precomputes)
   hgp_cand *cand;
   // scheduling
   const uint32_t *list;        // nodes of this launch (nullptr: every node of [lo,hi))

@@ -32,7 +32,7 @@ constexpr uint32_t flat_smem() {
 }
 
 template <int PIMAX>
-__global__ void __launch_bounds__(kFThreads, 3) k_score_flat(ScoreJob J, const uint64_t *cv) {
+__global__ void __launch_bounds__(kFThreads, 3) k_score_flat(ScoreJob J, const uint64_t *cv, const uint2 *wmu) {
   extern __shared__ __align__(16) unsigned char dyn[];
   constexpr uint32_t NW = kFThreads / 32, S = 1u << kFLog, hmask = S - 1;
   __shared__ uint64_t s_tops[(NW + 1) * PIMAX];
@@ -246,8 +246,9 @@ __global__ void __launch_bounds__(kFThreads, 3) k_score_flat(ScoreJob J, const u
         e_nm = acc[sl];
         it = inter[sl];
       }
-      const uint64_t uni = (uint64_t)inn + J.in_mu[v] - it;          // |in(n) ∪ in(m)|
-      const bool ok = wn + J.node_w[v] <= J.omega && (J.delta == HGP_UNBOUNDED || uni <= J.delta);
+      const uint2 wm = __ldg(wmu + v);                               // (size(m), in_mu(m))
+      const uint64_t uni = (uint64_t)inn + wm.y - it;                // |in(n) ∪ in(m)|
+      const bool ok = wn + wm.x <= J.omega && (J.delta == HGP_UNBOUNDED || uni <= J.delta);
       if (!ok) { J.nbr[b0 + i] = v | kPurge; continue; }
       if (small && ((((e_nm + J.noise_cap) << 32) | v) <= thr)) continue;   // cannot enter the top-pi
       uint64_t sc = e_nm;
@@ -316,6 +317,11 @@ __global__ void __launch_bounds__(kFThreads, 3) k_score_flat(ScoreJob J, const u
   }
 }
 
+__global__ void k_pack_wmu2(const uint32_t *node_w, const uint32_t *in_mu, uint32_t N, uint2 *wmu) {
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
+    wmu[n] = make_uint2(node_w[n], in_mu[n]);
+}
+
 __global__ void k_edge_cv2(const uint64_t *edge_off, const uint32_t *edge_w, uint32_t E, uint32_t norm, uint64_t *cv) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
     const uint64_t we = (uint64_t)edge_w[e] << HGP_FP_SHIFT;   // Eq.5 term c(e), 2^-24 fixed point
@@ -337,8 +343,13 @@ hgp_status launch_score_flat(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t E) {
   if (st) return st;
   HGP_TRY(launch(c, "edge_cv", k_edge_cv2, dim3(E ? (div_up(E, 256) < 4096 ? div_up(E, 256) : 4096) : 0), dim3(256), 0,
                  J.edge_off, J.edge_w, E, J.norm, cv));
+  uint2 *wmu = scratch_raw<uint2>(c, J.N ? J.N : 1, &st);
+  if (st) return st;
+  HGP_TRY(launch(c, "pack_wmu", k_pack_wmu2, dim3(J.N ? (div_up(J.N, 256) < 4096 ? div_up(J.N, 256) : 4096) : 0), dim3(256),
+                 0, J.node_w, J.in_mu, J.N, wmu));
   const uint32_t grid = J.list ? 3u * c->sm_count : (nn < 3u * c->sm_count ? (nn ? nn : 1) : 3u * c->sm_count);
-  return launch(c, "score_F", k_score_flat<PIMAX>, dim3(grid), dim3(kFThreads), flat_smem(), J, (const uint64_t *)cv);
+  return launch(c, "score_F", k_score_flat<PIMAX>, dim3(grid), dim3(kFThreads), flat_smem(), J, (const uint64_t *)cv,
+                (const uint2 *)wmu);
 }
 
 template hgp_status launch_score_flat<4>(hgp_ctx *, ScoreJob, uint32_t, uint32_t);

@@ -335,3 +335,34 @@ def test_radix_incidence_matches_oracle(hgp, ctx, monkeypatch, name, make):
     cg, cnb, _ = hgp.coarsen_level(ctx, g, nb, hgp.params(64, 600, 4), None, m, gam)
     rr = ref.coarsen_level(rg, ref.unique_neighbors(rg), ref.params(64, 600, 4))
     assert_csr_equal(cg.to_host(), rr["coarse"], "a5 (radix)")
+
+
+@pytest.mark.parametrize("name,make,frac", [
+    ("snn-rand-big-nbhd", lambda: hgpgen.snn(8, layers=4, rows=40, cols=60, fanout=99, window=15, rewire=1.0), True),
+    ("vlsi-small", lambda: hgpgen.vlsi(6, 20000, 20000, dmax=1024, in_cap=600), False),
+])
+def test_fused_level0_sampled_first_tier(hgp, ctx, monkeypatch, name, make, frac):
+    """The fused call samples every 64th node in tier A first and starts the rest in tier M when
+    most samples overflow A's table (HGP_FUSED_SAMPLE_MIN lowers the size at which it samples):
+    the level is the same either way."""
+    monkeypatch.setenv("HGP_FUSED_SAMPLE_MIN", "128")
+    hg = make()
+    cap = hgpgen.default_noise_cap(hg)
+    omega, delta = (256, 4096) if name.startswith("snn") else (64, 600)
+    g = gpu_build(hgp, ctx, hg)
+    rg = ref.build_csr_hg(hg)
+    rnb = ref.unique_neighbors(rg)
+    rr = ref.coarsen_level(rg, rnb, ref.params(omega, delta, 4, noise_seed=2, noise_cap=cap))
+    m = torch.empty(g.N, dtype=torch.uint32, device="cuda")
+    gam = torch.empty(g.N, dtype=torch.uint32, device="cuda")
+    cand = hgp.empty_cand(g.N, 4)
+    ctx.profile_begin("nbr")
+    nb, cg, cnb, st = hgp.coarsen_level0(ctx, g, hgp.params(omega, delta, 4, noise_seed=2, noise_cap=cap), cand, m, gam)
+    ctx.profile_end()
+    used = ctx.profile_report()
+    assert ("nbrscore_M" in used) == frac or not frac, used
+    assert_nbrs_equal(nb.to_host(), rnb, "sampled nbrs+flags")
+    assert_cand_equal(hgp.cand_to_numpy(cand), rr["cand"])
+    assert np.array_equal(gam.cpu().numpy(), rr["gamma"])
+    assert_csr_equal(cg.to_host(), rr["coarse"], "sampled coarse")
+    assert_nbrs_equal(cnb.to_host(), rr["coarse_nb"], "sampled coarse nbrs")

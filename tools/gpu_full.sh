@@ -10,3 +10,5 @@ timeout 1200 ncu --set full --import-source on --clock-control none -k regex:k_n
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
 python tools/ncu_summary.py gpurun_out/nbr_full.ncu-rep > gpurun_out/nbr_summary.txt 2>&1
 cat gpurun_out/bench_c2.json
+bash tools/gpu_workloads.sh > gpurun_out/workloads.txt 2>&1
+cat gpurun_out/workloads.txt
