@@ -509,7 +509,7 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
                    0, F.S.lo, L.hn, kStride, sample, rest, cnt2));
     F.list = sample; F.list_count = cnt2; F.log2s = kFALog;
     F.defer_list = L.la; F.defer_count = L.ca;
-    HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
+    HGP_TRY(launch(c, "nbrscore_S", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
     uint32_t deferred = 0;
     HGP_TRY(read_back(c, L.ca, 4, &deferred));
     const uint32_t ns = (L.hn + kStride - 1) / kStride;
@@ -586,6 +586,10 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   // pool estimate: min(T, 24 P) scaled to the range; nodes that do not fit get a second, exact pool
   const double frac = g->N ? (double)nn / g->N : 1.0;
   uint64_t pool_cap = (uint64_t)((T < 24 * g->P ? T : 24 * g->P) * (frac < 1.0 ? 1.25 * frac : 1.0)) + nn;
+  // at most 2^34 entries (64 GB; C5's 24 P would be 96 GB); nodes that do not fit go to the exact
+  // second pool. (A cap from cudaMemGetInfo was measured to misfire: the caching allocator's
+  // reserved blocks read as used, the pool shrank and the level took the slow second-pool path.)
+  if (pool_cap > (1ull << 34)) pool_cap = 1ull << 34;
   // test hooks (tests/test_gpu_parity.py): a tiny first pool, or every node on the unfused path
   const char *tp = getenv("HGP_TEST_FUSED_POOL");
   if (tp) pool_cap = strtoull(tp, nullptr, 10);
