@@ -4,7 +4,8 @@
 // One CTA (256 threads) per node n with |N(n)| <= 2048:
 //  phase 0  sum and gcd of c(e) over I(n) (c(e) precomputed per edge); the node runs PACKED
 //           ((eta/g) << ib | inter in one u32, one native shared atomic per visit) when that is
-//           exact, else SPLIT (u32 eta + u32 inter, exact when sum c(e) < 2^32), else it goes to
+//           exact, else SPLIT (u32 eta + a u16 inter in half a u32 word, exact when sum c(e) < 2^32
+//           and in_mu(n) < 2^16: the halves never carry into each other), else it goes to
 //           the wide tier (64-bit eta) of score.cu.
 //  phase 1  the unflagged entries of N(n) are inserted as bins (and their slots recorded in
 //           N(n) order); n itself gets a bin so that self-visits need no test.
@@ -28,11 +29,11 @@ constexpr int kFLog = 12, kFThreads = 256;    // 4096 slots, <= 2048 neighbours
 constexpr uint32_t kFCap = 1u << (kFLog - 1);
 
 constexpr uint32_t flat_smem() {
-  return (4u << kFLog) + 2 * ((4u << kFLog) + 16) + 2 * kFCap + kFT * 24u;
+  return (4u << kFLog) + ((4u << kFLog) + 16) + ((2u << kFLog) + 16) + 2 * kFCap + kFT * 24u;
 }
 
 template <int PIMAX>
-__global__ void __launch_bounds__(kFThreads, 3) k_score_flat(ScoreJob J, const uint64_t *cv, const uint2 *wmu) {
+__global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const uint64_t *cv, const uint2 *wmu) {
   extern __shared__ __align__(16) unsigned char dyn[];
   constexpr uint32_t NW = kFThreads / 32, S = 1u << kFLog, hmask = S - 1;
   __shared__ uint64_t s_tops[(NW + 1) * PIMAX];
@@ -43,14 +44,14 @@ __global__ void __launch_bounds__(kFThreads, 3) k_score_flat(ScoreJob J, const u
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   uint32_t *keys = reinterpret_cast<uint32_t *>(dyn);
   uint32_t *acc = keys + S;                                         // [S + 4]: slot S = trash
-  uint32_t *inter = acc + S + 4;                                    // [S + 4] (SPLIT only)
-  uint16_t *nslot = reinterpret_cast<uint16_t *>(inter + S + 4);    // slot of N(n)[i] (kFCap)
+  uint32_t *inter = acc + S + 4;                                    // [S/2 + 4] u16 pairs (SPLIT only)
+  uint16_t *nslot = reinterpret_cast<uint16_t *>(inter + S / 2 + 4);  // slot of N(n)[i] (kFCap)
   uint4 *rowA = reinterpret_cast<uint4 *>(nslot + kFCap);
   uint2 *rowB = reinterpret_cast<uint2 *>(rowA + kFT);
   const uint32_t keys_s = smem_u32addr(keys), acc_s = smem_u32addr(acc), inter_s = smem_u32addr(inter);
   const uint32_t total = J.list_count ? *J.list_count : J.hi - J.lo;
-  for (uint32_t i = tid; i < S; i += kFThreads) { keys[i] = kEmpty; acc[i] = 0; inter[i] = 0; }
-  if (tid < 4) { acc[S + tid] = 0; inter[S + tid] = 0; }
+  for (uint32_t i = tid; i < S; i += kFThreads) { keys[i] = kEmpty; acc[i] = 0; if (i < S / 2) inter[i] = 0; }
+  if (tid < 4) { acc[S + tid] = 0; inter[S / 2 + tid] = 0; }
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = J.list ? J.list[t] : J.lo + t;
     uint64_t b0, b1;
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kFThreads, 3) k_score_flat(ScoreJob J, const u
     if (g == 0) g = 1;
     uint32_t ib = inn ? 32 - __clz(inn) : 0;
     const bool packed = (((unsigned __int128)(S1 / g + 1)) << ib) <= ((unsigned __int128)1 << 32);
-    if (!packed && S1 >= (1ull << 32)) {                            // wide tier (CTA-uniform)
+    if (!packed && (S1 >= (1ull << 32) || inn >= (1u << 16))) {     // wide tier (CTA-uniform)
       if (tid == 0) J.wide_list[atomicAdd(J.wide_count, 1u)] = n;
       __syncthreads();
       continue;
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(kFThreads, 3) k_score_flat(ScoreJob J, const u
           const bool hit = val[u] && kk[u] == m[u];
           if (hit) {
             red_add_u32(acc_s + 4 * sl[u], add[u]);
-            if (iad[u]) red_add_u32(inter_s + 4 * sl[u], iad[u]);
+            if (iad[u]) red_add_u32(inter_s + 4 * (sl[u] >> 1), iad[u] << (16 * (sl[u] & 1)));
           }
           val[u] = val[u] && !hit;                                   // val now marks the misses
           anym |= val[u];
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(kFThreads, 3) k_score_flat(ScoreJob J, const u
               k2 = lds_u32(keys_s + 4 * slot);
             }
             red_add_u32(acc_s + 4 * slot, add[u]);
-            if (iad[u]) red_add_u32(inter_s + 4 * slot, iad[u]);
+            if (iad[u]) red_add_u32(inter_s + 4 * (slot >> 1), iad[u] << (16 * (slot & 1)));
           }
         }
       };
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(kFThreads, 3) k_score_flat(ScoreJob J, const u
         it = x & imask;
       } else {
         e_nm = acc[sl];
-        it = inter[sl];
+        it = (inter[sl >> 1] >> (16 * (sl & 1))) & 0xFFFFu;
       }
       const uint2 wm = __ldg(wmu + v);                               // (size(m), in_mu(m))
       const uint64_t uni = (uint64_t)inn + wm.y - it;                // |in(n) ∪ in(m)|
@@ -311,9 +312,9 @@ __global__ void __launch_bounds__(kFThreads, 3) k_score_flat(ScoreJob J, const u
     // ---- reset the used slots
     for (uint32_t i = tid; i < cnt; i += kFThreads) {
       const uint32_t sl = nslot[i];
-      if (sl != 0xFFFFu) { keys[sl] = kEmpty; acc[sl] = 0; inter[sl] = 0; }
+      if (sl != 0xFFFFu) { keys[sl] = kEmpty; acc[sl] = 0; inter[sl >> 1] = 0; }   // both halves are ours to clear
     }
-    if (tid == 0) { keys[s_self] = kEmpty; acc[s_self] = 0; inter[s_self] = 0; acc[S] = 0; inter[S] = 0; }
+    if (tid == 0) { keys[s_self] = kEmpty; acc[s_self] = 0; inter[s_self >> 1] = 0; acc[S] = 0; inter[S / 2] = 0; }
   }
 }
 
@@ -347,7 +348,7 @@ hgp_status launch_score_flat(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t E) {
   if (st) return st;
   HGP_TRY(launch(c, "pack_wmu", k_pack_wmu2, dim3(J.N ? (div_up(J.N, 256) < 4096 ? div_up(J.N, 256) : 4096) : 0), dim3(256),
                  0, J.node_w, J.in_mu, J.N, wmu));
-  const uint32_t grid = J.list ? 3u * c->sm_count : (nn < 3u * c->sm_count ? (nn ? nn : 1) : 3u * c->sm_count);
+  const uint32_t grid = J.list ? 4u * c->sm_count : (nn < 4u * c->sm_count ? (nn ? nn : 1) : 4u * c->sm_count);
   return launch(c, "score_F", k_score_flat<PIMAX>, dim3(grid), dim3(kFThreads), flat_smem(), J, (const uint64_t *)cv,
                 (const uint2 *)wmu);
 }
