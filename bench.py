@@ -134,6 +134,13 @@ def measured_peaks() -> tuple[float, str]:
     return 6650.0, "fallback"
 
 
+def ncu_record(kernel: str, workload: str) -> dict:
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return {}
+    return json.load(open(p)).get(workload, {}).get(kernel) or {}
+
+
 def ncu_traffic(kernel: str, workload: str):
     """dram read+write bytes per launch of `kernel` from the committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -187,6 +194,24 @@ def run_reference(args, rank: int, world: int):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def issue_roofline(kernel: str, workload: str, ms_per_launch: float, clk: dict):
+    """The dominant kernel is bound by instruction issue, not HBM: its warp-
+    instruction count per launch (committed ncu capture) over its live CUDA-event time, against
+    4 warp-instructions / cycle / SM x SMs x the SM clock sampled during the timed region."""
+    rec = ncu_record(kernel, workload)
+    wi = rec.get("warp_instructions")
+    if not wi or not ms_per_launch:
+        return None
+    import torch
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    peak = 4.0 * sms * mhz * 1e6
+    achieved = wi / (ms_per_launch * 1e-3)
+    return {"bound": "issue", "unit": "warp-instructions/s", "achieved": achieved, "peak": peak,
+            "frac": achieved / peak, "warp_instructions_per_launch": wi,
+            "peak_derivation": f"4 issue slots/cycle/SM x {sms} SMs x {mhz:.0f} MHz (sampled)"}
 
 
 # ------------------------------------------------------------------------------------------ GPU arm
@@ -378,6 +403,7 @@ def main():
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "alg_bytes_per_launch": alg / launches_per_step, "ms_per_launch": per_launch_ms,
                      "traffic": ncu_traffic(dominant, args.workload)},
+        "issue_roofline": issue_roofline(dominant, args.workload, per_launch_ms, clk),
         "level": {"Nc": st["Nc"], "Ec": st["Ec"], "Pc": st["Pc"], "Vc": st["Vc"],
                   "matched_fraction": float((match.view(torch.int32) != -1).sum().item()) / N,
                   "matched_per_round": st["matched_per_round"], "purged": st["purged"],
