@@ -18,7 +18,8 @@ namespace hgp {
 // One CTA per node. MODE kModeP32: one u32 per bin packs (eta/g) << ib | inter, where g is the
 // gcd of the node's c(e) and ib = bits(in_mu(n)) (exact: inter <= in_mu(n) < 2^ib, and the
 // node qualifies only if (sum c / g + 1) << ib <= 2^32); a single native shared-memory atomic
-// add per pin visit. MODE kModeSplit: u32 eta + u32 inter per bin (exact when sum c(e) over I(n)
+// add per pin visit. MODE kModeSplit (not launched: score_flat.cu's first tier runs split
+// accumulators itself): u32 eta + u32 inter per bin (exact when sum c(e) over I(n)
 // < 2^32: the usual case once hyperedge sizes differ and the gcd is 1); two native atomics per
 // visit (the inter one only for dst pins of in-edges). MODE kModeWide: u64 eta (CAS loop) + u32
 // inter per bin, for everything else.
@@ -294,10 +295,9 @@ __global__ void k_score_check(const uint32_t *node_w, const uint32_t *in_mu, uin
 
 // tiers: A = 4096-slot shared table (<= 2048 entries, 32 KB), B = 16384 slots (<= 8192, 128 KB),
 // W = wide accumulators (4096 slots x 16 B = 64 KB), H = global-memory tables (any size, wide)
-static constexpr uint32_t kSALog = 12, kSAThreads = 128;
+static constexpr uint32_t kSALog = 12;   // capacity of the first tier (score_flat.cu) is 1 << (kSALog - 1)
 static constexpr uint32_t kSBLog = 14, kSBThreads = 256;
 static constexpr uint32_t kSWLog = 12, kSWThreads = 256;
-static constexpr uint32_t kSSLog = 12, kSSThreads = 256;   // split tier: 48 KB, 4 CTAs/SM
 
 template <int PIMAX>
 hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_deg, uint32_t *lists,
@@ -305,14 +305,10 @@ hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_
   hgp_status st = HGP_OK;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_score<kSAThreads, kModeP32, true, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (8 << kSALog) + 16);
     cudaFuncSetAttribute(k_score<kSBThreads, kModeP32, true, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (8 << kSBLog) + 16);
     cudaFuncSetAttribute(k_score<kSWThreads, kModeWide, true, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          16 << kSWLog);
-    cudaFuncSetAttribute(k_score<kSSThreads, kModeSplit, true, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (12 << kSSLog) + 32);
     attr = true;
   }
   uint32_t *bigA = lists, *wide = lists + nn, *huge = lists + 2 * (size_t)nn;
