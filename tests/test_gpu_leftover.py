@@ -62,18 +62,21 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("pi,noise", [(4, False), (2, True)])
 @pytest.mark.parametrize("name,make,omega,delta", CASES, ids=[c[0] for c in CASES])
-def test_level_and_hierarchy_with_leftover(hgp, ctx, name, make, omega, delta):
+def test_level_and_hierarchy_with_leftover(hgp, ctx, name, make, omega, delta, pi, noise):
     hg = make()
     g = gpu_build(hgp, ctx, hg)
     rg = ref.build_csr_hg(hg)
-    p = hgp.params(omega, delta, 4, flags=hgp.FLAG_LEFTOVER)
+    cap = hgpgen.default_noise_cap(hg) if noise else 0
+    p = hgp.params(omega, delta, pi, noise_seed=5, noise_cap=cap, flags=hgp.FLAG_LEFTOVER)
+    rp = ref.params(omega, delta, pi, noise_seed=5, noise_cap=cap)
     # unfused level (a3 on N(n)) and the fused level-0 path
     nb = hgp.unique_neighbors(ctx, g)
     m = torch.empty(g.N, dtype=torch.uint32, device="cuda")
     gam = torch.empty(g.N, dtype=torch.uint32, device="cuda")
     cg, cnb, _ = hgp.coarsen_level(ctx, g, nb, p, None, m, gam)
-    rr = ref.coarsen_level(rg, ref.unique_neighbors(rg), ref.params(omega, delta, 4), leftover=True)
+    rr = ref.coarsen_level(rg, ref.unique_neighbors(rg), rp, leftover=True)
     assert np.array_equal(m.cpu().numpy(), rr["match"])
     assert_csr_equal(cg.to_host(), rr["coarse"], "level with f2")
     m0 = torch.empty(g.N, dtype=torch.uint32, device="cuda")
@@ -83,6 +86,6 @@ def test_level_and_hierarchy_with_leftover(hgp, ctx, name, make, omega, delta):
     assert_nbrs_equal(cnb0.to_host(), rr["coarse_nb"], "fused level with f2")
     # whole hierarchy
     rho, cl, cln, levels = hgp.coarsen(ctx, g, p)
-    r = ref.coarsen(rg, ref.params(omega, delta, 4), leftover=True)
+    r = ref.coarsen(rg, rp, leftover=True)
     assert len(levels) == len(r["levels"]) and np.array_equal(rho.cpu().numpy(), r["rho"])
     assert_csr_equal(cl.to_host(), r["coarsest"], "coarsest with f2")
