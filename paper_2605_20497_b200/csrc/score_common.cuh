@@ -114,12 +114,12 @@ __device__ __forceinline__ void warp_topk_merge(const TopK<PIMAX> &top, uint32_t
 #pragma unroll
     for (int i = 0; i < PIMAX; ++i)
       if (i == (int)head) h = top.k[i];
-    uint64_t best = h;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t ob = __shfl_xor_sync(0xFFFFFFFFu, best, o);
-      best = ob > best ? ob : best;
-    }
+    // u64 max as two 32-bit warp reductions (REDUX): the largest high word (score), then the
+    // largest low word (id) among the lanes holding it
+    const uint32_t hi = (uint32_t)(h >> 32);
+    const uint32_t mhi = __reduce_max_sync(0xFFFFFFFFu, hi);
+    const uint32_t mlo = __reduce_max_sync(0xFFFFFFFFu, hi == mhi ? (uint32_t)h : 0u);
+    const uint64_t best = ((uint64_t)mhi << 32) | mlo;
     if (lane == 0) out[r] = best;
     if (best != 0 && h == best) ++head;
   }
