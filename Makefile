@@ -18,9 +18,13 @@ oracle/libhgp_ref.so: oracle/hgp_ref.cpp oracle/hgp_ref.h
 	g++ -O2 -fPIC -shared -std=c++17 -Wall -Wextra -o $@ $<
 
 cuda: $(PKG)/libhgp.so
-$(PKG)/libhgp.so: $(CU_SRCS) $(CU_HDRS)
-	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
-	  -Xptxas -warn-spills -Iinclude -shared -o $@ $(CU_SRCS) -lcudart
+CU_OBJS := $(patsubst $(CSRC)/%.cu,build/obj/%.o,$(CU_SRCS))
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -Xptxas -warn-spills -Iinclude
+build/obj/%.o: $(CSRC)/%.cu $(CU_HDRS)
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+$(PKG)/libhgp.so: $(CU_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS) -lcudart
 
 clean:
-	rm -f hgpgen/libhgpgen.so oracle/libhgp_ref.so $(PKG)/libhgp.so
+	rm -rf build hgpgen/libhgpgen.so oracle/libhgp_ref.so $(PKG)/libhgp.so

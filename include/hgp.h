@@ -28,10 +28,16 @@
  *  - Errors: every call returns an hgp_status; the first error wins and
  *    hgp_last_error() (thread-local) names the lowest offending edge/node index.
  *    No exceptions and no host fallback: without a CUDA device every call fails.
- *  - Synchronisation: hgp_build_csr, hgp_unique_neighbors, hgp_contract and
- *    hgp_coarsen_level synchronise the ctx stream (scan totals size their outputs);
- *    hgp_score_pairs and hgp_match only enqueue work (device-side errors of a4 are
- *    reported by the next synchronising call on the same ctx).
+ *  - Synchronisation: EVERY compute entry point synchronises the ctx stream before it
+ *    returns, because each one reads device values on the host: hgp_build_csr,
+ *    hgp_unique_neighbors, hgp_contract (scan totals size their outputs), hgp_score_pairs
+ *    (work totals pick the kernel tier; the infeasibility check of P:321 is returned as a
+ *    status), hgp_match (the per-round count of over-long best-child chains selects the
+ *    pointer-jumping fallback; the two-cycle check of P:546-547 is returned as a status).
+ *    Outputs are therefore complete and errors final when a call returns; callers overlap
+ *    work across ctxs on different streams, not within one call.
+ *  - Device: every call makes the ctx's device current for its duration and restores the
+ *    caller's current device before returning (hgp_ctx_create included).
  */
 #ifndef HGP_H
 #define HGP_H
@@ -154,6 +160,13 @@ HGP_API uint64_t hgp_launch_count(const hgp_ctx *ctx);
  * synchronises the stream when either side is pageable host memory. */
 HGP_API hgp_status hgp_copy(hgp_ctx *ctx, void *dst, const void *src, size_t bytes);
 HGP_API hgp_status hgp_sync(hgp_ctx *ctx);
+/* Explicit per-ctx options (tests and experiments; the library reads no environment variables).
+ * Results never depend on them. Names: "fused_sample_min" (level size from which the fused
+ * level-0 kernel first runs tier A on every 64th node; default 65536), "fused_pool_cap" (capacity of
+ * the fused kernel's first neighbour pool, 0 = automatic), "unfused" (1: every node takes the
+ * unfused a2 -> a3 path), "inc_radix" (1: incidence transpose by radix sort), "debug_sync" (1:
+ * synchronise and trace every launch on stderr). Unknown names and negative values: HGP_E_ARG. */
+HGP_API hgp_status hgp_ctx_set_option(hgp_ctx *ctx, const char *name, int64_t value);
 /* Instrumentation: from hgp_profile_begin on, every kernel launch whose internal name contains
  * name_filter (e.g. "score_A") is bracketed by CUDA events on the ctx stream; hgp_profile_end
  * synchronises and returns the summed device time (ms) and the number of such launches. */
@@ -172,12 +185,14 @@ HGP_API hgp_status hgp_unique_neighbors(hgp_ctx *ctx, const hgp_csr *g, uint32_t
 
 /* a3: for n in [nb->lo, nb->hi): eta/inter histogram over unflagged N(n), validity, noise,
  * purge flags set IN PLACE on nb (idempotent), top-pi valid neighbours by (score desc, id desc)
- * into cand rows lo..hi-1 of a caller [N][pi] array. Asynchronous. */
+ * into cand rows lo..hi-1 of a caller [N][pi] array. Synchronises; HGP_E_INFEASIBLE names the
+ * lowest node that alone exceeds Omega or Delta. */
 HGP_API hgp_status hgp_score_pairs(hgp_ctx *ctx, const hgp_csr *g, hgp_nbrs *nb, const hgp_params *p,
                                    hgp_cand *cand);
 
 /* a4: pi rounds of exact matching; match[N] symmetric partner or HGP_NONE;
- * matched_per_round: DEVICE [pi] pairs matched per round, or NULL. Asynchronous. */
+ * matched_per_round: DEVICE [pi] pairs matched per round, or NULL. Synchronises;
+ * HGP_E_INTERNAL names a node on a proposal cycle longer than 2 (cannot happen for cand from a3). */
 HGP_API hgp_status hgp_match(hgp_ctx *ctx, const hgp_cand *cand, uint32_t N, uint32_t pi,
                              uint32_t *match, uint32_t *matched_per_round);
 
@@ -230,7 +245,7 @@ HGP_API hgp_status hgp_leftover_pairs(hgp_ctx *ctx, const hgp_cand *cand, uint32
  * hgp_coarsen_level0, level l >= 1 by hgp_coarsen_level on the previous coarse CSR and coarse
  * neighbour lists, noise seed p->noise_seed + l (reading #3). Stops after the first level whose
  * coarse node count is <= ceil(W / Omega) (1 if Omega = HGP_UNBOUNDED; W = total size) or that
- * matched no pair (reading #20), or after max_levels (1..HGP_MAX_LEVELS) levels.
+ * formed no pair, by a4 or by f2 (N' = N; reading #20), or after max_levels (1..HGP_MAX_LEVELS) levels.
  *   rho        caller DEVICE [g0->N]: rho = gamma^L o ... o gamma^1, each level-0 node's node on
  *              the coarsest level (the initial partition's clusters)
  *   coarsest, coarsest_nb   library-owned coarsest level (free with hgp_csr_free / hgp_nbrs_free)

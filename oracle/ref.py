@@ -297,7 +297,8 @@ def coarsen(g0: Csr, p: CParams, max_levels: int = 64, leftover: bool = False) -
     """Multi-level driver, written out plainly: level l is
     coarsen_level on the previous level's coarse CSR and neighbour lists, with noise seed
     p.noise_seed + l (reading #3: "the driver passes seed+level"); it stops after the first level
-    whose coarse node count is <= stop_nodes(g0, Omega) or that matched no pair (reading #20), or
+    whose coarse node count is <= stop_nodes(g0, Omega) or that formed no pair, by a4 or by the f2
+    leftover pairing (N' = N; reading #20), or
     after max_levels levels. rho = gamma^L o ... o gamma^1 maps each level-0 node to its node on
     the coarsest level (the initial partition's clusters)."""
     g, nb = g0, unique_neighbors(g0)
@@ -313,6 +314,6 @@ def coarsen(g0: Csr, p: CParams, max_levels: int = 64, leftover: bool = False) -
         levels.append({"N": g.N, "E": g.E, "P": g.P, "Nc": cg.N, "Ec": cg.E, "Pc": cg.P,
                        "matched_per_round": per, "gamma": r["gamma"], "match": r["match"]})
         g, nb = cg, r["coarse_nb"]
-        if g.N <= stop or sum(per) == 0:
+        if g.N <= stop or cg.N == levels[-1]["N"]:   # no pair formed (a4 or f2): N' = N
             break
     return {"rho": rho, "levels": levels, "coarsest": g, "coarsest_nb": nb, "stop_nodes": stop}

@@ -171,8 +171,8 @@ struct IncBlockSeg {   // segment 2n = in(n), 2n+1 = out(n)
 // inc, in_mu and g->max_inc. Synchronises (reads max degree).
 hgp_status build_incidence(hgp_ctx *c, hgp_csr *g) {
   // The radix transpose (radix.cu) is exact and deterministic but measured slower on B200 at C2
-  // (a1 9.5 vs 7.4 ms: its first scatter pass runs at ~0.5 TB/s); opt in with HGP_INC_RADIX=1.
-  const bool radix_path = getenv("HGP_INC_RADIX") != nullptr;
+  // (a1 9.5 vs 7.4 ms: its first scatter pass runs at ~0.5 TB/s); opt in with hgp_ctx_set_option(ctx, "inc_radix", 1).
+  const bool radix_path = c->opt.inc_radix;
   if (radix_path && g->P < (1ull << 30) && g->N < (1u << 30)) return build_incidence_radix(c, g);
   hgp_status st = HGP_OK;
   const uint32_t N = g->N, E = g->E;
@@ -309,5 +309,5 @@ extern "C" hgp_status hgp_build_csr(hgp_ctx *c, const hgp_input *in, hgp_csr *ou
 }
 
 extern "C" void hgp_csr_free(hgp_ctx *c, hgp_csr *g) {
-  if (c && g) free_csr(c, g);
+  if (c && g) { DeviceGuard dg(c->device); free_csr(c, g); }
 }

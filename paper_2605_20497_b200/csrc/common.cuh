@@ -57,6 +57,14 @@ struct hgp_ctx {
   uint64_t *d_err = nullptr;       // [kErrSlots] device
   uint64_t *h_pin = nullptr;       // [64] pinned host staging
   cudaEvent_t ev[8] = {};
+  // explicit options (hgp_ctx_set_option; tests and experiments only — no environment variables)
+  struct Options {
+    uint64_t fused_sample_min = 65536;   // level sizes from which the fused kernel samples tier A first
+    uint64_t fused_pool_cap = 0;         // 0 = automatic; else the first pool's capacity (test hook)
+    bool unfused = false;                // every node on the unfused a2 -> a3 path (test hook)
+    bool inc_radix = false;              // a1/a5 incidence transpose by radix sort (measured slower)
+    bool debug_sync = false;             // serialise and trace every launch
+  } opt;
   // profiling: CUDA events around every launch whose name contains prof_filter
   std::string prof_filter;
   bool prof_on = false;
@@ -73,14 +81,37 @@ struct hgp_ctx {
 
 namespace hgp {
 
-// RAII guard for top-level API entry points: resets scratch at depth 0.
+// Makes the ctx's device current for the scope and restores the caller's device on exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; cudaGetLastError(); }
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  DeviceGuard(const DeviceGuard &) = delete;
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// RAII guard for top-level API entry points: the ctx's device is current inside the call (the
+// caller's is restored), and scratch is reset at depth 0.
 struct ApiScope {
   hgp_ctx *c;
-  explicit ApiScope(hgp_ctx *c_) : c(c_) {
+  DeviceGuard dg;
+  explicit ApiScope(hgp_ctx *c_) : c(c_), dg(c_->device) {
     if (c->depth++ == 0) c->reset_scratch();
   }
   ~ApiScope() { --c->depth; }
 };
+
+// True exactly once per (flag word, device): per-device one-time setup such as
+// cudaFuncSetAttribute, which applies to the current device only.
+inline bool once_per_device(uint64_t *mask, int dev) {
+  const unsigned long long bit = 1ull << (dev & 63);
+  return (__atomic_fetch_or(reinterpret_cast<unsigned long long *>(mask), bit, __ATOMIC_ACQ_REL) & bit) == 0;
+}
 
 #define HGP_CUDA(x)                                                                              \
   do {                                                                                           \
@@ -100,7 +131,7 @@ template <class K, class... Args>
 inline hgp_status launch(hgp_ctx *c, const char *name, K kernel, dim3 grid, dim3 block, size_t smem,
                          Args... args) {
   if (grid.x == 0 || grid.y == 0 || grid.z == 0) return HGP_OK;
-  static const bool dbg = getenv("HGP_DEBUG_SYNC") != nullptr;   // debugging: serialise + trace
+  const bool dbg = c->opt.debug_sync;   // debugging: serialise + trace
   const bool prof = (c->prof_on && strstr(name, c->prof_filter.c_str()) != nullptr) || dbg;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (prof) { e0 = c->prof_event(); e1 = c->prof_event(); cudaEventRecord(e0, c->stream); }

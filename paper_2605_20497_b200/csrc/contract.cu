@@ -495,13 +495,12 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
   unsigned long long *misc = scratch_zero<unsigned long long>(c, 2, &st);   // purged, max bound (tier C)
   if (st) return st;
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_dev = 0;   // per device: cudaFuncSetAttribute applies to the current one
+  if (once_per_device(&attr_dev, c->device)) {
     cudaFuncSetAttribute(k_coarse_nbrs<kCAThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kCALog);
     // tiers M and B share the instantiation <256, true>: the attribute is the larger table's
     static_assert(kCMThreads == kCBThreads && kCMLog < kCBLog, "M and B share one instantiation");
     cudaFuncSetAttribute(k_coarse_nbrs<kCBThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kCBLog);
-    attr = true;
   }
   CNbrJob J{};
   J.mem0 = mem0; J.mem1 = mem1; J.nb_off = seg_off; J.gamma = gamma; J.bound_off = bound_off;

@@ -130,7 +130,7 @@ hgp_status hgp_ctx_create(int device, hgp_stream_t stream, const hgp_allocator *
     return set_error(HGP_E_CUDA, "hgp_ctx_create: no CUDA device (%s); there is no host fallback",
                      cudaGetErrorString(e));
   if (device < 0 || device >= ndev) return set_error(HGP_E_ARG, "hgp_ctx_create: bad device %d", device);
-  HGP_CUDA(cudaSetDevice(device));
+  DeviceGuard dg(device);   // the caller's current device is restored on return
   cudaDeviceProp prop;
   HGP_CUDA(cudaGetDeviceProperties(&prop, device));
   if (prop.major < 10)
@@ -165,7 +165,7 @@ hgp_status hgp_ctx_create(int device, hgp_stream_t stream, const hgp_allocator *
 
 void hgp_ctx_destroy(hgp_ctx *c) {
   if (!c) return;
-  cudaSetDevice(c->device);
+  DeviceGuard dg(c->device);
   cudaStreamSynchronize(c->stream);
   for (auto &ch : c->chunks) c->dfree(ch.p, ch.bytes);
   c->chunks.clear();
@@ -183,6 +183,7 @@ uint64_t hgp_launch_count(const hgp_ctx *c) { return c ? c->launches : 0; }
 hgp_status hgp_copy(hgp_ctx *c, void *dst, const void *src, size_t bytes) {
   if (!c || (!dst && bytes) || (!src && bytes)) return set_error(HGP_E_ARG, "hgp_copy: null argument");
   if (!bytes) return HGP_OK;
+  DeviceGuard dg(c->device);
   HGP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
   cudaPointerAttributes a{}, b{};
   cudaPointerGetAttributes(&a, dst);
@@ -206,6 +207,7 @@ hgp_status hgp_profile_begin(hgp_ctx *c, const char *name_filter) {
 hgp_status hgp_profile_end(hgp_ctx *c, double *total_ms, uint64_t *launches) {
   if (!c) return set_error(HGP_E_ARG, "hgp_profile_end: null ctx");
   c->prof_on = false;
+  DeviceGuard dg(c->device);
   HGP_CUDA(cudaStreamSynchronize(c->stream));
   double tot = 0;
   for (auto &pr : c->prof_events) {
@@ -220,6 +222,7 @@ hgp_status hgp_profile_end(hgp_ctx *c, double *total_ms, uint64_t *launches) {
 
 hgp_status hgp_profile_report(hgp_ctx *c, char *buf, size_t len) {
   if (!c || !buf || !len) return set_error(HGP_E_ARG, "hgp_profile_report: bad argument");
+  DeviceGuard dg(c->device);
   HGP_CUDA(cudaStreamSynchronize(c->stream));
   std::vector<std::pair<std::string, std::pair<double, uint64_t>>> acc;
   for (size_t i = 0; i < c->prof_events.size(); ++i) {
@@ -244,7 +247,21 @@ hgp_status hgp_profile_report(hgp_ctx *c, char *buf, size_t len) {
 
 hgp_status hgp_sync(hgp_ctx *c) {
   if (!c) return set_error(HGP_E_ARG, "hgp_sync: null ctx");
+  DeviceGuard dg(c->device);
   HGP_CUDA(cudaStreamSynchronize(c->stream));
+  return HGP_OK;
+}
+
+hgp_status hgp_ctx_set_option(hgp_ctx *c, const char *name, int64_t value) {
+  if (!c || !name) return set_error(HGP_E_ARG, "hgp_ctx_set_option: null argument");
+  if (value < 0) return set_error(HGP_E_ARG, "hgp_ctx_set_option: %s must be >= 0", name);
+  const std::string k = name;
+  if (k == "fused_sample_min") c->opt.fused_sample_min = (uint64_t)value;
+  else if (k == "fused_pool_cap") c->opt.fused_pool_cap = (uint64_t)value;
+  else if (k == "unfused") c->opt.unfused = value != 0;
+  else if (k == "inc_radix") c->opt.inc_radix = value != 0;
+  else if (k == "debug_sync") c->opt.debug_sync = value != 0;
+  else return set_error(HGP_E_ARG, "hgp_ctx_set_option: unknown option '%s'", name);
   return HGP_OK;
 }
 

@@ -480,22 +480,20 @@ struct TierLists {
 
 template <int PIMAX, int TA, int MINB>
 hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_dev = 0;   // per device: cudaFuncSetAttribute applies to the current one
+  if (once_per_device(&attr_dev, c->device)) {
     cudaFuncSetAttribute(k_nbrscore<TA, PIMAX, MINB, kFALog>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused_smem(kFALog));
     cudaFuncSetAttribute(k_nbrscore<kFMThreads, PIMAX, 3, kFMLog>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          fused_smem(kFMLog));
     cudaFuncSetAttribute(k_nbrscore<kFBThreads, PIMAX, 1, kFBLog>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          fused_smem(kFBLog));
-    attr = true;
   }
   const uint32_t sm = c->sm_count;
   const uint32_t per_sm = MINB;                                     // exactly the resident CTAs
   const uint32_t gA = L.hn < per_sm * sm ? L.hn : per_sm * sm;
   if (gA == 0) return HGP_OK;
   constexpr uint32_t kStride = 64;
-  const char *smin = getenv("HGP_FUSED_SAMPLE_MIN");                // test hook: sample small levels too
-  const uint32_t sample_min = smin ? (uint32_t)strtoul(smin, nullptr, 10) : 1024 * kStride;
+  const uint64_t sample_min = c->opt.fused_sample_min;            // 1024 * kStride by default
   if (!L.in_list && L.hn >= sample_min && L.hn >= 2 * kStride) {
     // Tier A on every 64th node first: if most of them overflow its table (large neighbourhoods,
     // e.g. the rewired SNN), the other nodes start in tier M instead of paying a wasted traversal
@@ -537,9 +535,7 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
 
 template <int PIMAX>
 hgp_status fused_tiers(hgp_ctx *c, FusedJob F, const TierLists &L) {
-  static const int cfg = getenv("HGP_FUSED_CFG") ? atoi(getenv("HGP_FUSED_CFG")) : 1;
-  if (cfg == 3) return fused_tiers_t<PIMAX, 256, 5>(c, F, L);   // 48 registers, 5 CTAs/SM
-  return fused_tiers_t<PIMAX, 256, 4>(c, F, L);                   // 64 registers, 4 CTAs/SM (measured faster)
+  return fused_tiers_t<PIMAX, 256, 4>(c, F, L);   // 64 registers, 4 CTAs/SM (measured faster than 48 / 5)
 }
 
 __global__ void k_list_cnt_sum(const uint32_t *list, const uint32_t *count, const uint32_t *cnt, uint32_t lo,
@@ -590,10 +586,10 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   // second pool. (A cap from cudaMemGetInfo was measured to misfire: the caching allocator's
   // reserved blocks read as used, the pool shrank and the level took the slow second-pool path.)
   if (pool_cap > (1ull << 34)) pool_cap = 1ull << 34;
-  // test hooks (tests/test_gpu_parity.py): a tiny first pool, or every node on the unfused path
-  const char *tp = getenv("HGP_TEST_FUSED_POOL");
-  if (tp) pool_cap = strtoull(tp, nullptr, 10);
-  const bool all_unfused = getenv("HGP_TEST_UNFUSED") != nullptr;
+  // test hooks (tests/test_gpu_parity.py, hgp_ctx_set_option): a tiny first pool, or every node
+  // on the unfused path
+  if (c->opt.fused_pool_cap) pool_cap = c->opt.fused_pool_cap;
+  const bool all_unfused = c->opt.unfused;
   if (pool_cap == 0) pool_cap = 1;
   uint32_t *pool = scratch_raw<uint32_t>(c, pool_cap, &st);
   if (st) return st;

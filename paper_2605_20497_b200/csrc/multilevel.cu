@@ -5,7 +5,7 @@
 // (which carry the OR-propagated purge flags, reading #7). Level l uses noise seed
 // p->noise_seed + l (reading #3: "the driver passes seed+level"). The driver stops after the
 // first level whose coarse node count is <= ceil(W / Omega) (1 when Omega is unbounded), or that
-// matched no pair (reading #20), or after max_levels levels. rho = gamma^L o ... o
+// formed no pair — by a4 or by f2 — i.e. N' = N (reading #20), or after max_levels levels. rho = gamma^L o ... o
 // gamma^1 (the initial partition's clusters) is composed on the device.
 #include "csr_impl.cuh"
 
@@ -35,6 +35,7 @@ extern "C" hgp_status hgp_coarsen(hgp_ctx *c, const hgp_csr *g0, const hgp_param
                                   uint32_t *levels_out) {
   if (!c || !g0 || !p || !rho || !coarsest || !coarsest_nb || !levels_out)
     return set_error(HGP_E_ARG, "hgp_coarsen: null argument");
+  DeviceGuard dg(c->device);
   if (max_levels < 1 || max_levels > HGP_MAX_LEVELS) return set_error(HGP_E_ARG, "hgp_coarsen: max_levels must be in [1,64]");
   if (g0->N == 0) return set_error(HGP_E_ARG, "hgp_coarsen: empty hypergraph");
   if (p->pi < 1 || p->pi > HGP_MAX_PI) return set_error(HGP_E_ARG, "pi must be in [1,16]");
@@ -84,7 +85,6 @@ extern "C" hgp_status hgp_coarsen(hgp_ctx *c, const hgp_csr *g0, const hgp_param
       ApiScope scope(c);
       s = launch(c, "compose", k_compose, dim3(grid), dim3(256), 0, rho, (const uint32_t *)gamma, N0);
     }
-    (void)nl;
     if (own) { free_csr(c, &cur); free_nbrs(c, &cur_nb); }
     cur = nxt;
     cur_nb = nxt_nb;
@@ -92,9 +92,8 @@ extern "C" hgp_status hgp_coarsen(hgp_ctx *c, const hgp_csr *g0, const hgp_param
     if (stats) stats[lvl] = ls;
     *levels_out = lvl + 1;
     if (s != HGP_OK) break;
-    uint64_t matched = 0;
-    for (int i = 0; i < HGP_MAX_PI; ++i) matched += ls.matched_per_round[i];
-    if ((uint64_t)cur.N <= stop || matched == 0) break;
+    // no pair formed on this level (a4 rounds and, with HGP_FLAG_LEFTOVER, f2 pairs alike): N' = N
+    if ((uint64_t)cur.N <= stop || cur.N == nl) break;
   }
   release();
   if (s != HGP_OK) {

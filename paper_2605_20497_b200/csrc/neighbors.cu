@@ -241,11 +241,10 @@ hgp_status nbrs_for_list(hgp_ctx *c, const hgp_csr *g, uint32_t lo, const uint32
   uint64_t hb[2];
   HGP_TRY(read_back(c, misc, 16, hb));
   *max_deg_out = (uint32_t)hb[1];
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_dev = 0;   // per device: cudaFuncSetAttribute applies to the current one
+  if (once_per_device(&attr_dev, c->device)) {
     cudaFuncSetAttribute(k_nbrs<kT1ThreadsL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT1LogL);
     cudaFuncSetAttribute(k_nbrs<kT2ThreadsL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT2LogL);
-    attr = true;
   }
   uint32_t *gtab = nullptr;
   uint32_t lg = 1;
@@ -328,11 +327,10 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
   uint32_t *pool = scratch_raw<uint32_t>(c, pool_cap, &st);
   if (st) return st;
 
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_dev = 0;   // per device: cudaFuncSetAttribute applies to the current one
+  if (once_per_device(&attr_dev, c->device)) {
     cudaFuncSetAttribute(k_nbrs<kT1Threads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT1Log);
     cudaFuncSetAttribute(k_nbrs<kT2Threads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kT2Log);
-    attr = true;
   }
   // Run the three tiers with a given pool; returns pool-overflow count and the pool cursor
   // (= exact total of unique entries once every node has deduplicated).
@@ -403,5 +401,5 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
 }
 
 extern "C" void hgp_nbrs_free(hgp_ctx *c, hgp_nbrs *nb) {
-  if (c && nb) free_nbrs(c, nb);
+  if (c && nb) { DeviceGuard dg(c->device); free_nbrs(c, nb); }
 }

@@ -303,13 +303,12 @@ template <int PIMAX>
 hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_deg, uint32_t *lists,
                               uint32_t *counts, const uint32_t *first_list, const uint32_t *first_count) {
   hgp_status st = HGP_OK;
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_dev = 0;   // per device: cudaFuncSetAttribute applies to the current one
+  if (once_per_device(&attr_dev, c->device)) {
     cudaFuncSetAttribute(k_score<kSBThreads, kModeP32, true, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (8 << kSBLog) + 16);
     cudaFuncSetAttribute(k_score<kSWThreads, kModeWide, true, PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          16 << kSWLog);
-    attr = true;
   }
   uint32_t *bigA = lists, *wide = lists + nn, *huge = lists + 2 * (size_t)nn;
   // F (score_flat.cu): every node with |N(n)| <= 2048, packed or split accumulators; larger

@@ -334,10 +334,9 @@ __global__ void k_edge_cv2(const uint64_t *edge_off, const uint32_t *edge_w, uin
 // |N(n)| <= 2048; larger neighbourhoods -> big_list, nodes needing 64-bit eta -> wide_list.
 template <int PIMAX>
 hgp_status launch_score_flat(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t E) {
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_dev = 0;   // per device: cudaFuncSetAttribute applies to the current one
+  if (once_per_device(&attr_dev, c->device)) {
     cudaFuncSetAttribute(k_score_flat<PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, flat_smem());
-    attr = true;
   }
   hgp_status st = HGP_OK;
   uint64_t *cv = scratch_raw<uint64_t>(c, E ? E : 1, &st);

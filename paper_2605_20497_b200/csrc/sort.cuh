@@ -192,10 +192,9 @@ hgp_status segmented_sort(hgp_ctx *c, Seg seg, uint64_t nseg, uint32_t *keys, ui
   if (st != HGP_OK) return st;
   HGP_TRY(launch(c, "segsort_warp", k_segsort_warp<Seg>, dim3(grid), dim3(kSortWarpsPerCta * 32), 0, seg, nseg,
                  keys, big, cnt));
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_dev = 0;
+  if (once_per_device(&attr_dev, c->device)) {
     cudaFuncSetAttribute(k_segsort_cta<Seg>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSortCap * 4);
-    attr_set = true;
   }
   HGP_TRY(launch(c, "segsort_cta", k_segsort_cta<Seg>, dim3(2 * c->sm_count), dim3(kCtaSortThreads),
                  kCtaSortCap * 4, seg, (const uint64_t *)big, (const uint32_t *)cnt, keys, huge, cnt + 1));

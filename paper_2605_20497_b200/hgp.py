@@ -8,6 +8,7 @@ call raises.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 from dataclasses import dataclass
@@ -103,6 +104,8 @@ def lib():
         L.hgp_launch_count.restype = ctypes.c_uint64
         L.hgp_copy.argtypes = [vp, vp, vp, ctypes.c_size_t]
         L.hgp_sync.argtypes = [vp]
+        L.hgp_ctx_set_option.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
+        L.hgp_ctx_set_option.restype = S
         L.hgp_profile_begin.argtypes = [vp, ctypes.c_char_p]
         L.hgp_profile_end.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]
         L.hgp_profile_begin.restype = S
@@ -216,6 +219,24 @@ class Ctx:
 
     def sync(self):
         _check(lib().hgp_sync(self.h))
+
+    OPTION_DEFAULTS = {"fused_sample_min": 65536, "fused_pool_cap": 0, "unfused": 0, "inc_radix": 0,
+                       "debug_sync": 0}
+
+    def set_option(self, name: str, value: int):
+        """hgp_ctx_set_option (tests / experiments; results never depend on options)."""
+        _check(lib().hgp_ctx_set_option(self.h, name.encode(), int(value)))
+
+    @contextlib.contextmanager
+    def options(self, **kw):
+        """Set options for a with-block and restore their defaults afterwards."""
+        for k, v in kw.items():
+            self.set_option(k, v)
+        try:
+            yield self
+        finally:
+            for k in kw:
+                self.set_option(k, self.OPTION_DEFAULTS[k])
 
     def profile_begin(self, name_filter: str):
         _check(lib().hgp_profile_begin(self.h, name_filter.encode()))

@@ -286,10 +286,12 @@ def test_fused_level0_partial_paths(hgp, ctx, monkeypatch, mode, name, make, ome
     """The fused call's secondary paths give the same level: a first pool too small for most nodes
     (second, exact pool), and every node on the unfused list path (k_nbrs + k_score over the
     segment view) — both with and without returning N(n)."""
-    if mode.startswith("pool"):
-        monkeypatch.setenv("HGP_TEST_FUSED_POOL", mode[4:])
-    else:
-        monkeypatch.setenv("HGP_TEST_UNFUSED", "1")
+    opts = {"fused_pool_cap": int(mode[4:])} if mode.startswith("pool") else {"unfused": 1}
+    with ctx.options(**opts):
+        _partial_paths(hgp, ctx, mode, make, omega, delta)
+
+
+def _partial_paths(hgp, ctx, mode, make, omega, delta):
     hg = make()
     cap = hgpgen.default_noise_cap(hg)
     g = gpu_build(hgp, ctx, hg)
@@ -322,9 +324,13 @@ def test_fused_level0_partial_paths(hgp, ctx, monkeypatch, mode, name, make, ome
                                        ("snn-small", lambda: hgpgen.snn(5, layers=4, rows=20, cols=20, fanout=30,
                                                                          window=9, rewire=0.1))])
 def test_radix_incidence_matches_oracle(hgp, ctx, monkeypatch, name, make):
-    """a1 with the radix-sort transpose (HGP_INC_RADIX=1; 1, 2 or 3 passes by node count) builds the
+    """a1 with the radix-sort transpose (option inc_radix; 1, 2 or 3 passes by node count) builds the
     same canonical incidence as the oracle, and so does a5's coarse incidence."""
-    monkeypatch.setenv("HGP_INC_RADIX", "1")
+    with ctx.options(inc_radix=1):
+        _radix(hgp, ctx, make)
+
+
+def _radix(hgp, ctx, make):
     hg = make()
     g = gpu_build(hgp, ctx, hg)
     rg = ref.build_csr_hg(hg)
@@ -343,9 +349,13 @@ def test_radix_incidence_matches_oracle(hgp, ctx, monkeypatch, name, make):
 ])
 def test_fused_level0_sampled_first_tier(hgp, ctx, monkeypatch, name, make, frac):
     """The fused call samples every 64th node in tier A first and starts the rest in tier M when
-    most samples overflow A's table (HGP_FUSED_SAMPLE_MIN lowers the size at which it samples):
+    most samples overflow A's table (option fused_sample_min lowers the size at which it samples):
     the level is the same either way."""
-    monkeypatch.setenv("HGP_FUSED_SAMPLE_MIN", "128")
+    with ctx.options(fused_sample_min=128):
+        _sampled(hgp, ctx, name, make, frac)
+
+
+def _sampled(hgp, ctx, name, make, frac):
     hg = make()
     cap = hgpgen.default_noise_cap(hg)
     omega, delta = (256, 4096) if name.startswith("snn") else (64, 600)

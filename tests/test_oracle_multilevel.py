@@ -24,25 +24,29 @@ CASES = [
 
 
 @pytest.mark.parametrize("name,make,omega,delta", CASES, ids=[c[0] for c in CASES])
-@pytest.mark.parametrize("cap", [0, 1 << 22])
-def test_hierarchy_invariants(name, make, omega, delta, cap):
+@pytest.mark.parametrize("cap,leftover", [(0, False), (1 << 22, False), (1 << 22, True)])
+def test_hierarchy_invariants(name, make, omega, delta, cap, leftover):
     hg = make()
     g0 = ref.build_csr_hg(hg)
-    r = ref.coarsen(g0, ref.params(omega, delta, 4, noise_seed=3, noise_cap=cap))
+    r = ref.coarsen(g0, ref.params(omega, delta, 4, noise_seed=3, noise_cap=cap), leftover=leftover)
     levels, rho, gl = r["levels"], r["rho"], r["coarsest"]
     W = int(hg.node_w.astype(np.int64).sum())
     stop = 1 if omega == ref.UNBOUNDED else -(-W // omega)
     assert r["stop_nodes"] == stop
     # stop rule: the last level stops, no earlier one does
     last = levels[-1]
-    assert last["Nc"] <= stop or sum(last["matched_per_round"]) == 0 or len(levels) == 64
+    # (a level that formed no pair, by a4 or by f2, has N' = N)
+    assert last["Nc"] <= stop or last["Nc"] == last["N"] or len(levels) == 64
     for lv in levels[:-1]:
-        assert lv["Nc"] > stop and sum(lv["matched_per_round"]) > 0
-    # N_{l+1} = N_l - matched pairs, and levels chain
+        assert lv["Nc"] > stop and lv["Nc"] < lv["N"]
+    # N_{l+1} = N_l - pairs formed (a4 pairs, plus f2 pairs with leftover), and levels chain
     for a, b in zip(levels, levels[1:]):
         assert b["N"] == a["Nc"] and b["E"] == a["Ec"] and b["P"] == a["Pc"]
     for lv in levels:
-        assert lv["Nc"] == lv["N"] - sum(lv["matched_per_round"])
+        pairs = int(np.count_nonzero(lv["match"] != ref.NONE)) // 2
+        assert lv["Nc"] == lv["N"] - pairs
+        if not leftover:
+            assert pairs == sum(lv["matched_per_round"])
     assert len(levels) >= 2
     # rho onto [0, N_L); sizes conserved; Omega / Delta on the original edges
     Nl = gl.N
