@@ -38,8 +38,9 @@ struct FusedJob {
   const uint2 *wmu;                       // [N] (size, in_mu) packed for the validity test
 };
 
-// Phase 2b + 3 of k_nbrscore. PACKED: every score of the node is < 2^32, so (score, id) is
-// one u64 key (exact order, one compare).
+// Phase 2b + 3 of k_nbrscore over the node's dense slot list. PACKED: every score of the node is
+// < 2^32 (S1 + cap < 2^32), so (score, id) is one u64 key and every sum and compare of the
+// validity test fits 32-bit arithmetic: sizes sum to < 2^32 (reading #2), |in(n) ∪ in(m)| <= E.
 template <int PIMAX, int THREADS, bool PACKED>
 __device__ __forceinline__ void eval_top(const ScoreJob &J, const FusedJob &F, uint32_t n, uint32_t count,
                                          const uint32_t *keys, const uint32_t *acc, const uint16_t *ulist, uint64_t g,
@@ -51,36 +52,49 @@ __device__ __forceinline__ void eval_top(const ScoreJob &J, const FusedJob &F, u
 #pragma unroll
   for (int i = 0; i < PIMAX; ++i) { top.s[i] = 0; top.id[i] = 0; topk.k[i] = 0; }
   uint64_t thr = 0;                                                // topk.k[pi - 1]
-  const uint64_t wn = J.node_w[n];
+  const uint32_t wn = J.node_w[n];
   const uint32_t inn = J.in_mu[n];
   const uint32_t imask = ib ? (uint32_t)((1ull << ib) - 1) : 0u;
-  for (uint32_t i = tid; i < count; i += THREADS) {
+  const uint32_t om32 = J.omega >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)J.omega;
+  const uint32_t de32 = J.delta >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)J.delta;   // HGP_UNBOUNDED too
+  const uint32_t g32 = (uint32_t)g, cap32 = (uint32_t)J.noise_cap;                  // PACKED only
+  auto visit = [&](uint32_t i, uint32_t &e_nm, uint32_t &v, bool &ok, uint64_t &sc64) {
     const uint32_t slot = ulist[i];
-    const uint32_t v = keys[slot];
+    v = keys[slot];
     const uint32_t x = acc[slot];
-    const uint64_t e_nm = (uint64_t)(ib < 32 ? x >> ib : 0) * g;
-    const uint64_t inter = x & imask;
+    const uint32_t cnt = ib < 32 ? x >> ib : 0u;
+    const uint32_t inter = x & imask;
     const uint2 wm = __ldg(F.wmu + v);                             // (size(m), in_mu(m)): one gather
-    const uint64_t uni = (uint64_t)inn + wm.y - inter;             // |in(n) ∪ in(m)|
-    const bool ok = wn + wm.x <= J.omega && (J.delta == HGP_UNBOUNDED || uni <= J.delta);
+    // |in(n) ∪ in(m)| = in_mu(n) + in_mu(m) - inter; inter <= in_mu(m)
+    ok = wn + wm.x <= om32 && inn + (wm.y - inter) <= de32;
     F.pool[base + i] = ok ? v : (v | kPurge);
+    e_nm = cnt * g32;                                              // PACKED: eta(n,m) < 2^32
+    sc64 = (uint64_t)cnt * g;
+  };
+  for (uint32_t i = tid; i < count; i += THREADS) {
+    uint32_t e_nm, v; bool ok; uint64_t sc;
+    visit(i, e_nm, v, ok, sc);
     if (!ok) continue;
-    // packed keys: even the largest noise cannot lift (score, id) above the current pi-th best
-    if (PACKED && ((((e_nm + J.noise_cap) << 32) | v) <= thr)) continue;
-    uint64_t sc = e_nm;
-    if (J.noise_cap) {
-      const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
-      sc += __umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);   // uniform in [0, cap]
-    }
     if (PACKED) {
-      const uint64_t key = (sc << 32) | v;
-      if (key > thr) {                                             // most candidates stop here
+      // even the largest noise cannot lift (score, id) above the current pi-th best
+      if ((((uint64_t)(e_nm + cap32) << 32) | v) <= thr) continue;
+      uint32_t s32 = e_nm;
+      if (cap32) {
+        const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
+        s32 += (uint32_t)__umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);   // uniform in [0, cap]
+      }
+      const uint64_t key = ((uint64_t)s32 << 32) | v;
+      if (key > thr) {
         topk_insert<PIMAX>(topk, J.pi, key);
 #pragma unroll
         for (int q = 0; q < PIMAX; ++q)
           if (q == (int)J.pi - 1) thr = topk.k[q];
       }
     } else {
+      if (J.noise_cap) {
+        const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
+        sc += __umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);
+      }
       top_insert<PIMAX>(top, J.pi, sc, v);
     }
   }
@@ -124,11 +138,11 @@ __device__ __forceinline__ void eval_top(const ScoreJob &J, const FusedJob &F, u
   }
 }
 
-// Shared-memory layout of k_nbrscore: keys[S] | acc[S] | dense slot list u16[S/2] | edge rows
-// of the current tile (A: {pointer to pins[edge start] - flat start, flat start of dst(e), add of a
-// src pin}, B: {flat end, add of a dst pin}).
+// Shared-memory layout of k_nbrscore: keys[S] | acc[S] | dense slot list u16[S/2] | rows of the
+// current tile of incident edges: uint4 {flat end, pins index - flat start (mod 2^32), flat start
+// of dst(e), add of a src pin} and u32 {add of a dst pin}.
 constexpr uint32_t kKT = 128;     // incident edges per tile
-constexpr uint32_t fused_smem(uint32_t lg) { return (9u << lg) + kKT * 24u; }
+constexpr uint32_t fused_smem(uint32_t lg) { return (9u << lg) + kKT * 20u; }
 
 // predicated shared CAS: lanes with p == false return `dflt` without touching memory
 __device__ __forceinline__ uint32_t cas_u32_if(bool p, uint32_t a, uint32_t cmp, uint32_t val, uint32_t dflt) {
@@ -140,19 +154,28 @@ __device__ __forceinline__ uint32_t cas_u32_if(bool p, uint32_t a, uint32_t cmp,
   return old;
 }
 
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
 // One CTA per node n (grid-stride over the node list): the fused a2 + a3 traversal of I(n).
-//  phase 0  sum and gcd of c(e) over I(n): is the packed 32-bit accumulator exact?
-//  phase 1  per tile of kKT incident edges: edge rows in shared memory (block scan of |e|), then
-//           the tile's pins are one flat sequence split evenly over the warps (no idle lanes
-//           whatever |e|; each lane tracks its current edge). Per pin, straight-line and
-//           predicated: one shared load of the home slot; an empty home slot is claimed with one
-//           shared CAS (first visit); if the home slot then holds the key, the packed term is
-//           added with one native shared atomic. Only keys displaced by a collision (a fraction
-//           of a percent at load <= 1/4 with the multiplicative hash) take the divergent
-//           linear-probing path, entered by the warp only when some lane needs it.
-//  phase 2  dense list of the occupied slots (one sweep, block scan), then validity, purge
-//           flags, noise and top-Pi over it; N(n) to the pool.
-//  reset    only the slots used (the table is cleared once per CTA).
+//  prologue  the first tile's edge data in registers; one barrier-reduction (__syncthreads_or)
+//            tells whether every c(e) over I(n) equals the first one (the common case: then
+//            g = c(e), S1/g = |I(n)|, no gcd and no division); otherwise sum and gcd by a block
+//            reduction. Is the packed 32-bit accumulator (eta/g << ib | inter) exact?
+//  phase 1   per tile of kKT incident edges: edge rows in shared memory (block scan of |e|), then
+//            the tile's pins are one flat sequence split evenly over the warps (no idle lanes
+//            whatever |e|; each lane tracks its current edge). Per pin, straight-line: one
+//            shared load of the home slot and, if it holds the pin (the ~(1 - V/T) of visits
+//            that are repeats), one predicated native shared atomic add of the packed term.
+//            The rest (first visits: claim an empty slot by CAS and append it to the dense slot
+//            list; collision-displaced keys: linear probing) runs once per 128-pin window only
+//            if some lane of the warp needs it.
+//  phase 2   validity, purge flags, noise and top-Pi over the dense slot list; N(n) to the pool.
+//  reset     only the slots used (the table is cleared once per CTA).
+// Requires P < 2^32 (32-bit pin indices; the caller routes larger levels to the unfused path).
 template <int THREADS, int PIMAX, int MINB, int LOG2S>
 __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -162,83 +185,101 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
   __shared__ uint32_t s_topi[(NW + 1) * PIMAX];
   __shared__ uint64_t s_sum[NW], s_g[NW];
   __shared__ uint32_t s_wsum[NW];
-  __shared__ uint32_t s_defer, s_full, s_self;
+  __shared__ uint32_t s_full, s_self, s_defer;
   __shared__ unsigned long long s_start;
   const ScoreJob &J = F.S;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  constexpr uint32_t log2s = LOG2S, S = 1u << LOG2S, ucap = S / 2, hmask = S - 1;
+  constexpr uint32_t S = 1u << LOG2S, ucap = S / 2, hmask = S - 1;
   uint32_t *keys = reinterpret_cast<uint32_t *>(dyn);
   uint32_t *acc = keys + S;
   uint16_t *ulist = reinterpret_cast<uint16_t *>(acc + S);
-  uint4 *rowA = reinterpret_cast<uint4 *>(ulist + S / 2);
-  uint2 *rowB = reinterpret_cast<uint2 *>(rowA + kKT);
-  const uint32_t keys_s = smem_u32addr(keys), acc_s = smem_u32addr(acc);
+  uint4 *rows = reinterpret_cast<uint4 *>(ulist + S / 2);
+  uint32_t *rowd = reinterpret_cast<uint32_t *>(rows + kKT);
+  // shared-window addresses kept in registers (no rematerialisation inside the pin loop)
+  const uint32_t keys_s = opaque_u32(smem_u32addr(keys)), acc_s = keys_s + 4 * S;
+  const uint32_t rows_s = opaque_u32(smem_u32addr(rows)), rowd_s = rows_s + 16 * kKT;
   const uint32_t total = F.list_count ? *F.list_count : J.hi - J.lo;
   for (uint32_t i = tid; i < S / 4; i += THREADS) {
     reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     reinterpret_cast<uint4 *>(acc)[i] = make_uint4(0, 0, 0, 0);
   }
+  if (tid == 0) s_full = 0;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = F.list ? F.list[t] : J.lo + t;
     const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1], iin = i0 + J.inc_nin[n];
+    const uint64_t deg = i1 - i0;
     const uint32_t inn = J.in_mu[n];
-    // ---- phase 0: sum / gcd of c(e) over I(n); the first tile's edge data stays in registers
-    uint32_t te = 0, tlen = 0, tns = 0, tmu = 0;
+    // ---- prologue: the first tile's edge data stays in registers
+    const bool mine = tid < kKT && i0 + tid < i1;
+    uint32_t tlen = 0, tns = 0, tmu = 0;
     uint64_t ta = 0, tce = 0;
-    if (tid < kKT && i0 + tid < i1) {
-      te = J.inc[i0 + tid];
+    if (mine) {
+      const uint32_t te = J.inc[i0 + tid];
       ta = J.edge_off[te];
       tlen = (uint32_t)(J.edge_off[te + 1] - ta);
       tns = J.edge_nsrc[te];
       tce = F.cv[te];
       tmu = i0 + tid < iin ? J.edge_mu[te] : 0u;
     }
-    uint64_t sum = tce, gg = tce;
-    for (uint64_t k = i0 + kKT + tid; k < i1; k += THREADS) {
-      const uint64_t ce = F.cv[J.inc[k]];
-      sum += ce;
-      gg = gcd64(gg, ce);
-    }
+    const uint64_t c0 = deg ? F.cv[J.inc[i0]] : 0;                 // broadcast load
+    bool diff = mine && tce != c0;
+#pragma unroll 1
+    for (uint64_t k = i0 + kKT + tid; k < i1; k += THREADS) diff |= F.cv[J.inc[k]] != c0;
+    const uint32_t tincl = warp_incl_scan(tlen);                   // tile-0 scan of |e|
+    if (lane == 31) s_wsum[w] = tincl;
+    const bool nonuni = __syncthreads_or(diff) != 0;               // B1 (also: the table is clean)
+    uint64_t g, S1g;                                               // gcd of c(e), S1 / g
+    bool small;                                                    // S1 + cap < 2^32
+    if (!nonuni) {
+      g = c0 ? c0 : 1;
+      S1g = deg;
+      small = (unsigned __int128)c0 * deg + J.noise_cap < ((unsigned __int128)1 << 32);
+    } else {   // rare on SNN inputs: mixed edge sizes or weights
+      uint64_t sum = tce, gg = tce;
+#pragma unroll 1
+      for (uint64_t k = i0 + kKT + tid; k < i1; k += THREADS) {
+        const uint64_t ce = F.cv[J.inc[k]];
+        sum += ce;
+        gg = gcd64(gg, ce);
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-      const uint64_t og = __shfl_xor_sync(0xFFFFFFFFu, gg, o);
-      if (og != gg) gg = gcd64(gg, og);
-    }
-    if (lane == 0) { s_sum[w] = sum; s_g[w] = gg; }
-    __syncthreads();   // also: the table is clean (initial clear / previous node's reset)
-    uint64_t S1 = 0, g = 0;                                        // every thread, same values
+      for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+        const uint64_t og = __shfl_xor_sync(0xFFFFFFFFu, gg, o);
+        if (og != gg) gg = gcd64(gg, og);
+      }
+      if (lane == 0) { s_sum[w] = sum; s_g[w] = gg; }
+      __syncthreads();
+      uint64_t S1 = 0;
+      g = 0;
 #pragma unroll
-    for (uint32_t q = 0; q < NW; ++q) {
-      S1 += s_sum[q];
-      const uint64_t x = s_g[q];
-      if (x != g) g = gcd64(g, x);
+      for (uint32_t q = 0; q < NW; ++q) {
+        S1 += s_sum[q];
+        const uint64_t x = s_g[q];
+        if (x != g) g = gcd64(g, x);
+      }
+      if (g == 0) g = 1;
+      S1g = S1 / g;
+      small = (unsigned __int128)S1 + J.noise_cap < ((unsigned __int128)1 << 32);
     }
-    if (g == 0) g = 1;
     const uint32_t ib = inn ? 32 - __clz(inn) : 0;
-    const bool small = (unsigned __int128)S1 + J.noise_cap < ((unsigned __int128)1 << 32);
-    if ((((unsigned __int128)(S1 / g + 1)) << ib) > ((unsigned __int128)1 << 32)) {   // packed form inexact
+    if ((((unsigned __int128)(S1g + 1)) << ib) > ((unsigned __int128)1 << 32)) {   // packed form inexact
       if (tid == 0) F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
-      __syncthreads();                                             // s_sum / s_g are rewritten next
-      continue;
+      continue;                                                    // nothing was inserted
     }
     if (tid == 0) {
-      s_full = 0;
       bool ins = false;
-      s_self = hs_insert_slot(keys, log2s, n, &ins);              // self-visits land in n's slot
+      s_self = hs_insert_slot(keys, LOG2S, n, &ins);               // self-visits land in n's slot
     }
-    if (i1 == i0) __syncthreads();                                 // no tile barrier orders s_self
     // ---- phase 1, tile by tile
+    bool full = false;
     for (uint64_t t0 = i0; t0 < i1; t0 += kKT) {
       const uint32_t kt = (uint32_t)min((uint64_t)kKT, i1 - t0);
-      uint32_t len = 0, ns = 0, as = 0, ad = 0;
-      uint64_t a = 0;
-      if (tid < kt) {
-        uint64_t ce = tce;
-        uint32_t mu = tmu;
-        if (t0 == i0) {
-          a = ta; len = tlen; ns = tns;
-        } else {
+      uint32_t len = tlen, ns = tns, mu = tmu, incl = tincl;
+      uint64_t a = ta, ce = tce;
+      if (t0 != i0) {
+        len = 0; ns = 0; mu = 0; a = 0; ce = 0;
+        if (tid < kt) {
           const uint32_t e = J.inc[t0 + tid];
           a = J.edge_off[e];
           len = (uint32_t)(J.edge_off[e + 1] - a);
@@ -246,22 +287,20 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
           ce = F.cv[e];
           mu = t0 + tid < iin ? J.edge_mu[e] : 0u;
         }
-        as = (uint32_t)((ce == g ? 1ull : ce / g) << ib);
-        ad = as + mu;                                              // m in dst(e), e in in(n)
+        incl = warp_incl_scan(len);
+        if (lane == 31) s_wsum[w] = incl;
+        __syncthreads();
       }
-      const uint32_t incl = warp_incl_scan(len);
-      if (lane == 31) s_wsum[w] = incl;
-      __syncthreads();
       uint32_t woff = 0, tot = 0;
 #pragma unroll
       for (uint32_t q = 0; q < NW; ++q) { const uint32_t x = s_wsum[q]; woff += q < w ? x : 0u; tot += x; }
       if (tid < kt) {
         const uint32_t ex = woff + incl - len;
-        const uint64_t pp = reinterpret_cast<uint64_t>(J.pins + a) - 4ull * ex;   // &pins[a] - ex
-        rowA[tid] = make_uint4((uint32_t)pp, (uint32_t)(pp >> 32), ex + ns, as);
-        rowB[tid] = make_uint2(ex + len, ad);
+        const uint32_t as = (uint32_t)((nonuni && ce != g ? ce / g : 1ull) << ib);
+        rows[tid] = make_uint4(ex + len, (uint32_t)a - ex, ex + ns, as);
+        rowd[tid] = as + mu;                                       // m in dst(e), e in in(n)
       }
-      __syncthreads();
+      __syncthreads();                                             // B2: rows (and n's slot) visible
       // this warp's share of the tile's flat pin sequence
       const uint32_t flo = (uint32_t)(((uint64_t)tot * w) / NW), fhi = (uint32_t)(((uint64_t)tot * (w + 1)) / NW);
       uint32_t k = 0;
@@ -270,66 +309,82 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
         uint32_t lo_ = 0, hi_ = kt - 1;
         while (lo_ < hi_) {
           const uint32_t mid = (lo_ + hi_) >> 1;
-          if (rowB[mid].x > f) hi_ = mid; else lo_ = mid + 1;
+          if (rows[mid].x > f) hi_ = mid; else lo_ = mid + 1;
         }
         k = lo_;
       }
-      uint4 ra = rowA[k];
-      uint2 rb = rowB[k];
-      bool full = false;
+      uint4 ra = lds_v4(rows_s + 16 * k);
+      uint32_t rd = lds_u32(rowd_s + 4 * k);
+      // one 128-pin window of this warp's range; FULL: the window lies inside [flo, fhi)
       // one 128-pin window of this warp's range; FULL: the window lies inside [flo, fhi)
       auto window = [&](uint32_t f0, auto full_tag) {
         constexpr bool FULL = decltype(full_tag)::value;
-        uint32_t m[4], add[4], sl[4], kk[4];
+        uint32_t m[4], add[4], sl[4], kk[4], miss = 0;
         bool val[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t f = f0 + u * 32 + lane;
           val[u] = FULL || f < fhi;
           if (val[u]) {
-            while (f >= rb.x) { ++k; ra = rowA[k]; rb = rowB[k]; }   // next incident edge
+            while (f >= ra.x) { ++k; ra = lds_v4(rows_s + 16 * k); rd = lds_u32(rowd_s + 4 * k); }   // next edge
           }
-          const uint32_t *pf = reinterpret_cast<const uint32_t *>(((uint64_t)ra.y << 32) | ra.x) + f;
-          m[u] = val[u] ? __ldg(pf) : 0u;
-          add[u] = f >= ra.z ? rb.y : ra.w;
+          m[u] = val[u] ? __ldg(J.pins + (ra.y + f)) : 0u;
+          add[u] = f >= ra.z ? rd : ra.w;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          sl[u] = hash_slot(m[u], log2s);
+          sl[u] = hash_slot(m[u], LOG2S);
           kk[u] = lds_u32(keys_s + 4 * sl[u]);
         }
-        uint32_t any_miss = 0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          // valid: claim an empty home (CAS); hit if the home now holds m; add; else miss
-          uint32_t miss;
-          asm volatile(
-              "{\n .reg .pred pv, pc, ph;\n .reg .b32 o;\n"
-              " setp.ne.u32 pv, %2, 0;\n"
-              " setp.eq.and.u32 pc, %3, -1, pv;\n"
-              " mov.b32 o, %3;\n"
-              " @pc atom.shared.cas.b32 o, [%1], -1, %4;\n"
-              " setp.eq.u32 ph, o, %4;\n"
-              " setp.eq.or.u32 ph, o, -1, ph;\n"
-              " and.pred ph, ph, pv;\n"
-              " selp.u32 o, %5, 0, ph;\n"                       // a miss adds 0 to the
-              " red.shared.add.u32 [%1+%6], o;\n"               // slot it looked at: no branch
-              " not.pred ph, ph;\n"
-              " and.pred ph, ph, pv;\n"
-              " selp.u32 %0, 1, 0, ph;\n}"
-              : "=r"(miss)
-              : "r"(keys_s + 4 * sl[u]), "r"((uint32_t)val[u]), "r"(kk[u]), "r"(m[u]), "r"(add[u]), "n"(4 * S)
-              : "memory");
-          val[u] = miss != 0;                                      // val now marks the misses
-          any_miss |= miss;
+          // claim an empty home (CAS; a first visit); hit if the home now holds m; add the packed
+          // term — a miss adds 0 to the slot it looked at (no branch); else report a miss
+          uint32_t ms;
+          if (FULL) {
+            asm volatile(
+                "{\n .reg .pred pc, ph;\n .reg .b32 o;\n"
+                " setp.eq.u32 pc, %2, -1;\n"
+                " mov.b32 o, %2;\n"
+                " @pc atom.shared.cas.b32 o, [%1], -1, %3;\n"
+                " setp.eq.u32 ph, o, %3;\n"
+                " setp.eq.or.u32 ph, o, -1, ph;\n"
+                " selp.u32 o, %4, 0, ph;\n"
+                " red.shared.add.u32 [%1+%5], o;\n"
+                " selp.u32 %0, 0, 1, ph;\n}"
+                : "=r"(ms)
+                : "r"(keys_s + 4 * sl[u]), "r"(kk[u]), "r"(m[u]), "r"(add[u]), "n"(4 * S)
+                : "memory");
+          } else {
+            asm volatile(
+                "{\n .reg .pred pv, pc, ph;\n .reg .b32 o;\n"
+                " setp.ne.u32 pv, %2, 0;\n"
+                " setp.eq.and.u32 pc, %3, -1, pv;\n"
+                " mov.b32 o, %3;\n"
+                " @pc atom.shared.cas.b32 o, [%1], -1, %4;\n"
+                " setp.eq.u32 ph, o, %4;\n"
+                " setp.eq.or.u32 ph, o, -1, ph;\n"
+                " and.pred ph, ph, pv;\n"
+                " selp.u32 o, %5, 0, ph;\n"
+                " red.shared.add.u32 [%1+%6], o;\n"
+                " not.pred ph, ph;\n"
+                " and.pred ph, ph, pv;\n"
+                " selp.u32 %0, 1, 0, ph;\n}"
+                : "=r"(ms)
+                : "r"(keys_s + 4 * sl[u]), "r"((uint32_t)val[u]), "r"(kk[u]), "r"(m[u]), "r"(add[u]), "n"(4 * S)
+                : "memory");
+          }
+          miss |= ms << u;
         }
-        if (__any_sync(0xFFFFFFFFu, any_miss != 0)) {              // displaced keys: probe on
+        if (__any_sync(0xFFFFFFFFu, miss != 0)) {                  // collision-displaced keys: probe on
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            if (!val[u]) continue;
+            if (!((miss >> u) & 1u)) continue;
             uint32_t slot = sl[u], probes = 0, k2;
+            bool ok = true;
+#pragma unroll 1
             do {
-              if (++probes > kProbeCap) { full = true; break; }
+              if (++probes > kProbeCap) { ok = false; break; }
               slot = (slot + 1) & hmask;
               k2 = lds_u32(keys_s + 4 * slot);
               if (k2 == kEmpty) {
@@ -337,7 +392,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
                 if (k2 == kEmpty) break;
               }
             } while (k2 != m[u]);
-            if (!full) red_add_u32(acc_s + 4 * slot, add[u]);
+            if (ok) red_add_u32(acc_s + 4 * slot, add[u]);
+            else full = true;
           }
         }
       };
@@ -345,47 +401,34 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       for (; f0 + 128 <= fhi; f0 += 128) window(f0, std::true_type{});
       if (f0 < fhi) window(f0, std::false_type{});
       if (full) s_full = 1;
-      __syncthreads();                                             // rows are rewritten by the next tile
+      __syncthreads();                                             // B3: rows are rewritten next
       if (s_full) break;
     }
-    // ---- phase 2a: dense list of the occupied slots (but n's): S / THREADS (<= 64) slots per thread
-    constexpr uint32_t kPer = S / THREADS;
-    using Occ = typename std::conditional<(kPer <= 32), uint32_t, uint64_t>::type;
-    Occ occ = 0;
-    const uint32_t s0 = tid * kPer;
-#pragma unroll
-    for (uint32_t j = 0; j < kPer; j += 4) {
-      const uint4 kv = *reinterpret_cast<const uint4 *>(keys + s0 + j);
-      occ |= (Occ)((uint32_t)(kv.x != kEmpty) | (uint32_t)(kv.y != kEmpty) << 1 | (uint32_t)(kv.z != kEmpty) << 2 |
-                   (uint32_t)(kv.w != kEmpty) << 3)
-             << j;
+    if (deg == 0) __syncthreads();                                 // no tile barrier orders s_self
+    // ---- phase 2a: dense list of the occupied slots (but n's) by a ballot sweep; warp w owns the
+    //      slots [w S/NW, (w+1) S/NW): pass 1 counts, pass 2 (after the block's counts) writes
+    constexpr uint32_t SW = S / NW;
+    const uint32_t self = s_self, wbase = w * SW;
+    uint32_t wc = 0;
+    for (uint32_t j = 0; j < SW; j += 32) {
+      const uint32_t slot = wbase + j + lane;
+      wc += __popc(__ballot_sync(0xFFFFFFFFu, keys[slot] != kEmpty && slot != self));
     }
-    if (s_self - s0 < kPer) occ &= ~((Occ)1 << (s_self - s0));
-    const uint32_t c1 = sizeof(Occ) == 4 ? __popc((uint32_t)occ) : __popcll((uint64_t)occ), ci = warp_incl_scan(c1);
-    if (lane == 31) s_wsum[w] = ci;
-    __syncthreads();
+    if (lane == 0) s_wsum[w] = wc;
+    __syncthreads();                                               // B3'
     uint32_t woff = 0, count = 0;
 #pragma unroll
     for (uint32_t q = 0; q < NW; ++q) { const uint32_t x = s_wsum[q]; woff += q < w ? x : 0u; count += x; }
     if (s_full || count > ucap) {                                  // table too small: next tier
-      __syncthreads();
-      if (tid == 0) F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
+      __syncthreads();                                             // every thread has read s_full / s_wsum
+      if (tid == 0) { F.defer_list[atomicAdd(F.defer_count, 1u)] = n; s_full = 0; }
       for (uint32_t i = tid; i < S / 4; i += THREADS) {
         reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
         reinterpret_cast<uint4 *>(acc)[i] = make_uint4(0, 0, 0, 0);
       }
-      continue;                                                    // phase 0's barrier orders the clear
+      continue;                                                    // B1 of the next node orders the clear
     }
-    {
-      uint32_t pos = woff + ci - c1;
-      Occ x = occ;
-      while (x) {
-        const uint32_t j = sizeof(Occ) == 4 ? __ffs((int)(uint32_t)x) - 1 : __ffsll((long long)x) - 1;
-        x &= x - 1;
-        ulist[pos++] = (uint16_t)(s0 + j);
-      }
-    }
-    // ---- phase 2b: pool space for N(n), then validity / flags / noise / top-pi
+    // ---- phase 2b: pool space for N(n) (thread 0) while the warps write the dense list
     if (tid == 0) {
       s_defer = 0;
       const unsigned long long st = atomicAdd(F.pool_cursor, (unsigned long long)count);
@@ -398,13 +441,20 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
         F.start[n - J.lo] = st + F.start_bias;
       }
     }
-    __syncthreads();
+    for (uint32_t j = 0; j < SW; j += 32) {
+      const uint32_t slot = wbase + j + lane;
+      const bool occ = keys[slot] != kEmpty && slot != self;
+      const uint32_t b = __ballot_sync(0xFFFFFFFFu, occ);
+      if (occ) ulist[woff + __popc(b & ((1u << lane) - 1))] = (uint16_t)slot;
+      woff += __popc(b);
+    }
+    __syncthreads();                                               // B4
+    if (tid == 0) s_full = 0;
     if (!s_defer) {
       if (small) eval_top<PIMAX, THREADS, true>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
       else eval_top<PIMAX, THREADS, false>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
     }
-    __syncthreads();
-    // ---- reset the used slots
+    // ---- reset the used slots (eval's barrier: every warp is done reading them)
     for (uint32_t i = tid; i < count; i += THREADS) {
       const uint32_t sl = ulist[i];
       keys[sl] = kEmpty;
@@ -575,6 +625,7 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   uint32_t *lists = scratch_raw<uint32_t>(c, 4 * (size_t)(nn ? nn : 1), &st);
   if (st) return st;
   if (nn == 0) return HGP_E_INTERNAL;   // handled by the caller's fallback
+  if (g->P >= (1ull << 32)) return HGP_E_INTERNAL;   // the fused kernel indexes pins with 32 bits
   HGP_TRY(launch(c, "pairs_total", k_pairs_total, dim3(g->E ? (div_up(g->E, 256) < 1024 ? div_up(g->E, 256) : 1024) : 0),
                  dim3(256), 0, (const uint64_t *)g->edge_off, g->E, misc));
   uint64_t T = 0;
