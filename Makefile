@@ -14,8 +14,8 @@ hgpgen/libhgpgen.so: hgpgen/hgpgen.c hgpgen/hgpgen.h
 	gcc -O2 -fPIC -shared -std=c11 -Wall -Wextra -o $@ $< -lm
 
 oracle: oracle/libhgp_ref.so
-oracle/libhgp_ref.so: oracle/hgp_ref.cpp oracle/hgp_ref.h
-	g++ -O2 -fPIC -shared -std=c++17 -Wall -Wextra -o $@ $<
+oracle/libhgp_ref.so: oracle/hgp_ref.cpp oracle/hgp_ref_refine.cpp oracle/hgp_ref.h
+	g++ -O2 -fPIC -shared -std=c++17 -Wall -Wextra -o $@ oracle/hgp_ref.cpp oracle/hgp_ref_refine.cpp
 
 cuda: $(PKG)/libhgp.so
 CU_OBJS := $(patsubst $(CSRC)/%.cu,build/obj/%.o,$(CU_SRCS))

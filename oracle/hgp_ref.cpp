@@ -521,3 +521,6 @@ int hgp_ref_coarsen_level(const hgp_ref_csr *g, hgp_ref_nbrs *nb, const hgp_ref_
 }
 
 }  // extern "C"
+
+// error reporting for the next-row functions (hgp_ref_refine.cpp)
+int hgp_ref_set_error(int code, const char *msg) { return fail(code, "%s", msg); }

@@ -93,6 +93,50 @@ int  hgp_ref_contract(const hgp_ref_csr *g, const hgp_ref_nbrs *nb, const uint32
 int  hgp_ref_coarsen_level(const hgp_ref_csr *g, hgp_ref_nbrs *nb, const hgp_ref_params *p,
                            hgp_ref_cand *cand, uint32_t *match, uint32_t *gamma,
                            hgp_ref_csr *coarse, hgp_ref_nbrs *coarse_nb);
+/* ---- next rows: f1 partition quality, f3 refinement gains, f4 validation ----
+ * part: [N] partition id of every node (rho), every id < nparts. Plain definitions
+ * written out; see oracle/hgp_ref_refine.cpp for the passages each follows. */
+typedef struct {
+  uint64_t connectivity;         /* Eq.1: sum_e omega(e) (lambda(e) - 1) */
+  uint64_t cut_net;              /* Eq.16: sum_e omega(e) [lambda(e) > 1] */
+  uint64_t max_size;             /* max_p |p| = sum_{n: rho(n)=p} size(n) */
+  uint64_t max_inbound;          /* max_p sum_{e: dst(e) meets p} mu(e) (reading #12) */
+  uint32_t size_violations;      /* partitions with |p| > Omega */
+  uint32_t inbound_violations;   /* partitions with inbound count > Delta */
+} hgp_ref_quality;
+int hgp_ref_partition_metrics(const hgp_ref_csr *g, const uint32_t *part, uint32_t nparts, uint64_t omega,
+                              uint64_t delta, hgp_ref_quality *out);
+
+/* f3: sparse pins(p, e): per edge e the distinct partitions of its pins in
+ * ascending id with their counts; inbound = 1 counts dst(e) pins only (pins_in). */
+typedef struct {
+  uint32_t E;
+  uint64_t nnz;
+  uint64_t *off;                 /* [E+1] */
+  uint32_t *part;                /* [nnz] ascending inside an edge */
+  uint32_t *count;               /* [nnz] >= 1 */
+} hgp_ref_pins;
+int hgp_ref_pins_matrix(const hgp_ref_csr *g, const uint32_t *part, int inbound, hgp_ref_pins *out);
+void hgp_ref_pins_free(hgp_ref_pins *pm);
+/* Eq.13 proposals: dest[n] = max_id argmax over p != rho(n) holding a pin of some
+ * e in I(n) of gain(n,p) = saving(n) - loss(n,p); HGP_REF_NONE if there is no such p (or none
+ * passes size(n) + |p| <= Omega when enforce_size). gain[n] = that gain (0 if none). */
+int hgp_ref_propose_moves(const hgp_ref_csr *g, const uint32_t *part, uint32_t nparts, uint64_t omega,
+                          int enforce_size, uint32_t *dest, int64_t *gain);
+/* In-sequence gains (Eqs.14-15): seq[0..M) distinct node ids, each with dest[seq[i]]
+ * != NONE; gain_seq[i] = connectivity before move i minus after it, with moves 0..i-1 applied. */
+int hgp_ref_in_sequence_gains(const hgp_ref_csr *g, const uint32_t *part, uint32_t nparts, const uint32_t *seq,
+                              uint32_t M, const uint32_t *dest, int64_t *gain_seq);
+/* f4: violations[i] = number of partitions with |p| > Omega or inbound count > Delta
+ * after moves 0..i of the sequence are applied. */
+int hgp_ref_sequence_violations(const hgp_ref_csr *g, const uint32_t *part, uint32_t nparts, const uint32_t *seq,
+                                uint32_t M, const uint32_t *dest, uint64_t omega, uint64_t delta,
+                                uint32_t *violations);
+/* The landing point: *k = the prefix length (1..M) with violations[k-1] == 0 and the
+ * largest cumulative in-sequence gain, the shortest on ties; *k = 0 (apply nothing) if that gain is
+ * <= 0 or no prefix is legal. *best = its cumulative gain (0 when *k = 0). */
+int hgp_ref_best_prefix(const int64_t *gain_seq, const uint32_t *violations, uint32_t M, uint32_t *k, int64_t *best);
+
 void hgp_ref_csr_free(hgp_ref_csr *g);
 void hgp_ref_nbrs_free(hgp_ref_nbrs *nb);
 const char *hgp_ref_last_error(void);

@@ -317,3 +317,101 @@ def coarsen(g0: Csr, p: CParams, max_levels: int = 64, leftover: bool = False) -
         if g.N <= stop or cg.N == levels[-1]["N"]:   # no pair formed (a4 or f2): N' = N
             break
     return {"rho": rho, "levels": levels, "coarsest": g, "coarsest_nb": nb, "stop_nodes": stop}
+
+
+# ----------------------------------------------------------------------------- next rows (§8(f))
+class CQuality(ctypes.Structure):
+    _fields_ = [("connectivity", ctypes.c_uint64), ("cut_net", ctypes.c_uint64), ("max_size", ctypes.c_uint64),
+                ("max_inbound", ctypes.c_uint64), ("size_violations", ctypes.c_uint32),
+                ("inbound_violations", ctypes.c_uint32)]
+
+
+class CPins(ctypes.Structure):
+    _fields_ = [("E", ctypes.c_uint32), ("nnz", ctypes.c_uint64), ("off", u64p), ("part", u32p), ("count", u32p)]
+
+
+i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+def _lib2():
+    L = lib()
+    if not hasattr(L, "_refine_typed"):
+        cp = ctypes.POINTER(CCsr)
+        L.hgp_ref_partition_metrics.argtypes = [cp, u32p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                                ctypes.POINTER(CQuality)]
+        L.hgp_ref_pins_matrix.argtypes = [cp, u32p, ctypes.c_int, ctypes.POINTER(CPins)]
+        L.hgp_ref_pins_free.argtypes = [ctypes.POINTER(CPins)]
+        L.hgp_ref_propose_moves.argtypes = [cp, u32p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, u32p, i64p]
+        L.hgp_ref_in_sequence_gains.argtypes = [cp, u32p, ctypes.c_uint32, u32p, ctypes.c_uint32, u32p, i64p]
+        L.hgp_ref_sequence_violations.argtypes = [cp, u32p, ctypes.c_uint32, u32p, ctypes.c_uint32, u32p,
+                                                  ctypes.c_uint64, ctypes.c_uint64, u32p]
+        L.hgp_ref_best_prefix.argtypes = [i64p, u32p, ctypes.c_uint32, u32p, i64p]
+        for f in (L.hgp_ref_partition_metrics, L.hgp_ref_pins_matrix, L.hgp_ref_propose_moves,
+                  L.hgp_ref_in_sequence_gains, L.hgp_ref_sequence_violations, L.hgp_ref_best_prefix):
+            f.restype = ctypes.c_int
+        L._refine_typed = True
+    return L
+
+
+def _u32(a):
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+def partition_metrics(g: Csr, part, nparts: int, omega: int = UNBOUNDED, delta: int = UNBOUNDED) -> dict:
+    """f1: Eq.1 connectivity, Eq.16 cut-net and the constraint loads of a partition of g."""
+    part = _u32(part)
+    q = CQuality()
+    cg = g._c()
+    _check(_lib2().hgp_ref_partition_metrics(ctypes.byref(cg), _ptr(part, u32p), nparts, omega, delta,
+                                             ctypes.byref(q)))
+    return {k: int(getattr(q, k)) for k, _ in CQuality._fields_}
+
+
+def pins_matrix(g: Csr, part, inbound: bool = False):
+    """f3: per edge the sorted (partition, count) pairs of pins(p, e) (or pins_in). Returns (off, part, count)."""
+    part = _u32(part)
+    out = CPins()
+    cg = g._c()
+    _check(_lib2().hgp_ref_pins_matrix(ctypes.byref(cg), _ptr(part, u32p), int(inbound), ctypes.byref(out)))
+    res = (_arr(out.off, out.E + 1, np.uint64), _arr(out.part, out.nnz, np.uint32), _arr(out.count, out.nnz, np.uint32))
+    _lib2().hgp_ref_pins_free(ctypes.byref(out))
+    return res
+
+
+def propose_moves(g: Csr, part, nparts: int, omega: int = UNBOUNDED, enforce_size: bool = False):
+    """f3: Eq.13 proposals. Returns (dest [N] u32, NONE = no move; gain [N] i64)."""
+    part = _u32(part)
+    dest = np.zeros(g.N, dtype=np.uint32)
+    gain = np.zeros(g.N, dtype=np.int64)
+    cg = g._c()
+    _check(_lib2().hgp_ref_propose_moves(ctypes.byref(cg), _ptr(part, u32p), nparts, omega, int(enforce_size),
+                                         _ptr(dest, u32p), gain.ctypes.data_as(i64p)))
+    return dest, gain
+
+
+def in_sequence_gains(g: Csr, part, nparts: int, seq, dest) -> np.ndarray:
+    part, seq, dest = _u32(part), _u32(seq), _u32(dest)
+    out = np.zeros(len(seq), dtype=np.int64)
+    cg = g._c()
+    _check(_lib2().hgp_ref_in_sequence_gains(ctypes.byref(cg), _ptr(part, u32p), nparts, _ptr(seq, u32p), len(seq),
+                                             _ptr(dest, u32p), out.ctypes.data_as(i64p)))
+    return out
+
+
+def sequence_violations(g: Csr, part, nparts: int, seq, dest, omega: int, delta: int) -> np.ndarray:
+    part, seq, dest = _u32(part), _u32(seq), _u32(dest)
+    out = np.zeros(len(seq), dtype=np.uint32)
+    cg = g._c()
+    _check(_lib2().hgp_ref_sequence_violations(ctypes.byref(cg), _ptr(part, u32p), nparts, _ptr(seq, u32p),
+                                               len(seq), _ptr(dest, u32p), omega, delta, _ptr(out, u32p)))
+    return out
+
+
+def best_prefix(gain_seq, violations):
+    gs = np.ascontiguousarray(gain_seq, dtype=np.int64)
+    vi = _u32(violations)
+    k = ctypes.c_uint32()
+    b = ctypes.c_int64()
+    _check(_lib2().hgp_ref_best_prefix(gs.ctypes.data_as(i64p), _ptr(vi, u32p), len(gs), ctypes.byref(k),
+                                       ctypes.byref(b)))
+    return int(k.value), int(b.value)
