@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--hierarchy", action="store_true", help="run hgp_coarsen (all levels) instead of level 0")
     a = ap.parse_args()
     w = hgpgen.WORKLOADS[a.workload]
     hg = w.make(a.seed)
@@ -31,6 +32,15 @@ def main():
     cand = hgp.empty_cand(N, w.pi)
     m = torch.empty(N, dtype=torch.uint32, device="cuda")
     gam = torch.empty(N, dtype=torch.uint32, device="cuda")
+    if a.hierarchy:
+        for _ in range(a.steps):
+            g = hgp.build_csr(ctx, N, dev["edge_off"], dev["edge_nsrc"], dev["pins"], dev["edge_w"], dev["node_w"])
+            rho, cg, cnb, levels = hgp.coarsen(ctx, g, p)
+            print(len(levels), "levels", flush=True)
+            for x in (g, cg, cnb):
+                x.free()
+        torch.cuda.synchronize()
+        return
     for _ in range(a.steps):
         g = hgp.build_csr(ctx, N, dev["edge_off"], dev["edge_nsrc"], dev["pins"], dev["edge_w"], dev["node_w"])
         nb, cg, cnb, st = hgp.coarsen_level0(ctx, g, p, cand, m, gam)
