@@ -61,8 +61,8 @@ def algorithmic_bytes(step: str, N, E, P, V, pi, Nc=0, Ec=0, Pc=0, Vc=0) -> int:
         return 4 * V + 8 * P + 20 * E + 28 * N + 16 * pi * N
     if step == "a4":
         return 16 * pi * N + 4 * N
-    if step == "a2+a3":   # fused: a3's reads + the write of N(n) instead of its read
-        return 8 * P + 20 * E + 28 * N + 4 * V + 16 * pi * N
+    if step == "a2+a3":   # the fused kernel does both rows: charged their sum
+        return algorithmic_bytes("a2", N, E, P, V, pi) + algorithmic_bytes("a3", N, E, P, V, pi)
     if step == "a5":
         return 16 * N + 4 * P + 20 * E + 8 * Pc + 20 * Ec + 4 * V + 4 * Vc + 28 * Nc
     raise KeyError(step)
@@ -196,6 +196,25 @@ def run_reference(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def pin_visits(edge_off: np.ndarray) -> int:
+    """T = sum over e of |e| (|e| - 1): the pin visits of a2/a3's traversal (SURVEY §8 symbols)."""
+    d = np.diff(edge_off.astype(np.int64))
+    return int((d * (d - 1)).sum())
+
+
+def smem_roofline(visits_per_launch: float, ms_per_launch: float, clk: dict):
+    """The shared-memory roofline of the traversal: every pin visit needs at least
+    one 4-byte key load and one 4-byte atomic add in shared memory, 8 B through the 128 B/cycle/SM
+    crossbar (B300_MICROARCH "LDS/STS": 128/N B/cyc/SM, N = 1 without bank conflicts), so at most
+    16 visits per cycle per SM."""
+    import torch
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    peak = 16.0 * sms * mhz * 1e6
+    achieved = visits_per_launch / (ms_per_launch * 1e-3)
+    return achieved, peak, f"128 B/cycle/SM smem crossbar / 8 B per visit x {sms} SMs x {mhz:.0f} MHz (sampled)"
+
+
 def issue_roofline(kernel: str, workload: str, ms_per_launch: float, clk: dict):
     """The dominant kernel is bound by instruction issue, not HBM: its warp-
     instruction count per launch (committed ncu capture) over its live CUDA-event time, against
@@ -209,9 +228,58 @@ def issue_roofline(kernel: str, workload: str, ms_per_launch: float, clk: dict):
     mhz = (clk or {}).get("sm_mhz") or 1965.0
     peak = 4.0 * sms * mhz * 1e6
     achieved = wi / (ms_per_launch * 1e-3)
-    return {"bound": "issue", "unit": "warp-instructions/s", "achieved": achieved, "peak": peak,
+    return {"unit": "warp-instructions/s", "achieved": achieved, "peak": peak,
             "frac": achieved / peak, "warp_instructions_per_launch": wi,
             "peak_derivation": f"4 issue slots/cycle/SM x {sms} SMs x {mhz:.0f} MHz (sampled)"}
+
+
+def refine_leg(hgp, ctx, hierarchy, omega, delta, stream):
+    """SURVEY §8(f) on the bench input: f1 = Eq.1 / Eq.16 / loads of the initial partition rho of the
+    hierarchy on level 0; f3 + f4 = one refinement step on it, each call timed with CUDA
+    events: pins and pins_in matrices, Eq.13 proposals (size-enforcing), in-sequence
+    gains, event-based violations and the landing point. The move sequence is the proposals in
+    gain order (built untimed; the chaining of P:944-960 is not one of these rows). Applying the
+    landing prefix and re-measuring Eq.1 checks the whole step: Eq.1 must drop by exactly `best`."""
+    import torch
+    _, _, g, rho, cg = hierarchy(keep=True)
+    nparts = cg.N
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    t = {}
+
+    def timed(name, fn):
+        a, b = ev(), ev()
+        a.record(stream)
+        out = fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        t[name] = round(a.elapsed_time(b), 3)
+        return out
+
+    q = timed("f1_quality", lambda: hgp.partition_metrics(ctx, g, rho, nparts, omega, delta))
+    pins = timed("pins", lambda: hgp.pins_matrix(ctx, g, rho, nparts))
+    pins_in = timed("pins_in", lambda: hgp.pins_matrix(ctx, g, rho, nparts, inbound=True))
+    dest, gain = timed("propose_moves", lambda: hgp.propose_moves(ctx, g, rho, nparts, omega, True, pins=pins))
+    movers = torch.nonzero(dest.view(torch.int32) != -1).flatten()       # dest != NONE
+    order = torch.argsort(-gain[movers], stable=True)
+    seq = movers[order].to(torch.int32).contiguous()                     # u32 ids (int32 view)
+    gs = timed("in_sequence_gains", lambda: hgp.in_sequence_gains(ctx, g, rho, nparts, seq, dest, pins=pins))
+    vio = timed("sequence_violations",
+                lambda: hgp.sequence_violations(ctx, g, rho, nparts, seq, dest, omega, delta, pins_in=pins_in))
+    k, best = timed("best_prefix", lambda: hgp.best_prefix(ctx, gs, vio))
+    moved = rho.view(torch.int32).clone()
+    if k:
+        idx = seq[:k].long()
+        moved[idx] = dest.view(torch.int32)[idx]
+    q2 = hgp.partition_metrics(ctx, g, moved, nparts, omega, delta)
+    for x in (pins, pins_in, g, cg):
+        x.free()
+    out = {"what": "one refinement step on rho (f3 Eq.13 + Eqs.14-15, f4 P:1032-1057), GPU calls timed",
+           "nparts": nparts, "moves_proposed": int(seq.numel()), "landing_prefix": k, "gain": best,
+           "connectivity_before": q["connectivity"], "connectivity_after": q2["connectivity"],
+           "gain_checks": q["connectivity"] - q2["connectivity"] == best,
+           "violations_after": q2["size_violations"] + q2["inbound_violations"], "ms": t,
+           "total_ms": round(sum(t.values()), 3)}
+    return q, out
 
 
 # ------------------------------------------------------------------------------------------ GPU arm
@@ -225,6 +293,7 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-refine", action="store_true", help="skip the f1 quality / f3-f4 refinement-step leg")
     ap.add_argument("--dominant", default=None, help="kernel name for the roofline (default: measured top kernel)")
     args = ap.parse_args()
 
@@ -299,6 +368,9 @@ def main():
     ctx.profile_end()
     breakdown = ctx.profile_report()
     dominant = args.dominant or max(breakdown, key=lambda k: breakdown[k][0])
+    # the dominant kernel's family (every tier launch of it in a step, e.g. nbrscore_S/A/M/B):
+    # the step's algorithmic work is charged to their summed device time
+    family = dominant.split("_")[0] if dominant.split("_")[-1] in ("S", "A", "M", "B", "W", "H", "C") else dominant
 
     # ---- timed region: K steps, inputs resident in HBM (420 MB > 126 MB L2)
     clocks = ClockSampler(local)
@@ -308,7 +380,7 @@ def main():
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ctx.profile_begin(dominant)
+    ctx.profile_begin(family)
     ev0.record(stream)
     for _ in range(args.steps):
         step(dev)
@@ -346,11 +418,15 @@ def main():
 
     # ---- whole hierarchy: a1 + hgp_coarsen to the stop rule, 1 GPU, CUDA events
     hier = None
+    refine = None
     if world == 1:
-        def hierarchy():
+        def hierarchy(keep=False):
             g = hgp.build_csr(ctx, N, dev["edge_off"], dev["edge_nsrc"], dev["pins"], dev["edge_w"], dev["node_w"])
             rho, cg, cnb, levels = hgp.coarsen(ctx, g, params)
             out = (levels, cg.N)
+            if keep:
+                cnb.free()
+                return out + (g, rho, cg)
             for x in (g, cg, cnb):
                 x.free()
             return out
@@ -361,11 +437,14 @@ def main():
         h1.record(stream)
         torch.cuda.synchronize()
         hms = h0.elapsed_time(h1)
-        hier = {"what": "a1 + every level to the stop rule (hgp_coarsen, reading #20)", "levels": len(levels),
+        hier = {"what": "a1 + every level to the stop rule (hgp_coarsen, reading #21)", "levels": len(levels),
                 "total_coarsening_ms": hms, "pins_per_s": P / (hms / 1e3), "coarsest_nodes": n_last,
                 "level_ms": [round(l["ms"]["total"], 3) for l in levels],
                 "level_nodes": [l["N"] for l in levels],
                 "matched_fraction": [round(2 * sum(l["matched_per_round"]) / max(l["N"], 1), 4) for l in levels]}
+        if not args.no_refine:
+            hier_q, refine = refine_leg(hgp, ctx, hierarchy, omega, delta, stream)
+            hier["initial_partition"] = hier_q
 
     if rank != 0:
         if world > 1:
@@ -375,11 +454,26 @@ def main():
     V = last["V"]
     dstep = step_of(dominant)
     alg = algorithmic_bytes(dstep, N, E, P, V, pi, st["Nc"], st["Ec"], st["Pc"], st["Vc"])
-    per_launch_ms = dom_ms / max(dom_launches, 1)
-    # bytes per launch: the step's bytes split over that step's launches of this kernel per step
-    launches_per_step = max(dom_launches / args.steps, 1)
-    achieved = (alg / launches_per_step) / (per_launch_ms * 1e-3) / 1e9
+    fam_ms_step = dom_ms / args.steps                       # the family's device time per step
+    achieved = alg / (fam_ms_step * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
+    rec = ncu_record(dominant, args.workload)
+    hbm_view = {"achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                "alg_bytes_per_step": alg, "traffic": rec.get("dram_bytes_per_launch")}
+    roof = {"bound": "hbm", **hbm_view}
+    if dstep in ("a2+a3", "a3", "a2"):
+        # measured: the traversal kernels use a few % of DRAM bandwidth and most issue slots
+        # (profiles/ncu_traffic.json), so the binding roofline is the shared-memory visit rate
+        T = pin_visits(hg.edge_off)
+        va, vp, deriv = smem_roofline(T, fam_ms_step, clk)
+        measured_bound = "alu" if (rec.get("issue_pct") or 100.0) > (rec.get("dram_pct") or 0.0) else "hbm"
+        if measured_bound == "alu":
+            roof = {"bound": "alu", "achieved": va, "peak": vp, "unit": "pin-visits/s", "frac": va / vp,
+                    "visits_per_step": T, "peak_derivation": deriv, "traffic": rec.get("dram_bytes_per_launch"),
+                    "hbm": hbm_view}
+    roof.update({"kernel": dominant, "family": family, "step": dstep, "ms_per_step": fam_ms_step,
+                 "launches_per_step": dom_launches / args.steps,
+                 "ncu": {k: rec.get(k) for k in ("dram_pct", "issue_pct", "l2_hit_pct", "ipc_active")} if rec else None})
     # per step of the path from CUDA events around the API calls of the last step (a1 = hgp_build_csr;
     # a2+a3 / a4 / a5 = the level's own events, hgp_level_stats.ms), not from kernel-name guesses
     ea, eb = last["a1_events"]
@@ -399,11 +493,8 @@ def main():
                    "l2": "inputs (%.0f MB) larger than L2" % (h2d_bytes / 1e6)},
         "gpu_launches": launches,
         "clocks": clk,
-        "roofline": {"bound": "hbm", "kernel": dominant, "step": dstep, "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "alg_bytes_per_launch": alg / launches_per_step, "ms_per_launch": per_launch_ms,
-                     "traffic": ncu_traffic(dominant, args.workload)},
-        "issue_roofline": issue_roofline(dominant, args.workload, per_launch_ms, clk),
+        "roofline": roof,
+        "issue_roofline": issue_roofline(dominant, args.workload, fam_ms_step, clk),
         "level": {"Nc": st["Nc"], "Ec": st["Ec"], "Pc": st["Pc"], "Vc": st["Vc"],
                   "matched_fraction": float((match.view(torch.int32) != -1).sum().item()) / N,
                   "matched_per_round": st["matched_per_round"], "purged": st["purged"],
@@ -417,6 +508,8 @@ def main():
         line["e2e"] = e2e
     if hier:
         line["hierarchy"] = hier
+    if refine:
+        line["refine_step"] = refine
     if world == 1 and not args.no_cpu_baseline:
         hs, om, de, desc = oracle_sample(args.workload, args.seed, "baseline")
         t = oracle_level_seconds(hs, om, de, pi, hgpgen.default_noise_cap(hs), args.seed)

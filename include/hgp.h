@@ -256,6 +256,74 @@ HGP_API hgp_status hgp_coarsen(hgp_ctx *ctx, const hgp_csr *g0, const hgp_params
                                uint32_t *rho, hgp_csr *coarsest, hgp_nbrs *coarsest_nb, hgp_level_stats *stats,
                                uint32_t *levels_out);
 
+/* ---- rows after the level: f1 quality, f3 refinement gains, f4 validation ----
+ * A partition is part[N] (DEVICE) with ids < nparts; any id >= nparts is HGP_E_ARG naming the
+ * lowest such node. Every call synchronises. All sums are exact integers. */
+
+/* f1: quality of a partition (HOST struct). */
+typedef struct {
+  uint64_t connectivity;        /* Eq.1: sum over e of omega(e) (lambda(e) - 1) */
+  uint64_t cut_net;             /* Eq.16: sum of omega(e) over edges with lambda(e) > 1 */
+  uint64_t max_size;            /* max over p of sum of size(n), n in p */
+  uint64_t max_inbound;         /* max over p of sum of mu(e) over e with a dst pin in p */
+  uint32_t size_violations;     /* partitions with size > Omega */
+  uint32_t inbound_violations;  /* partitions with inbound load > Delta (never for HGP_UNBOUNDED) */
+} hgp_quality;
+
+/* f3: sparse pins(p, e) or pins_in(p, e): row e lists the distinct partitions
+ * of e's pins (of dst(e) only for pins_in) in ascending id with their pin counts. Library-owned
+ * DEVICE arrays, released with hgp_pins_free. lambda(e) = off[e+1] - off[e] for the full matrix. */
+typedef struct {
+  uint32_t E, pad_;
+  uint64_t nnz;
+  uint64_t *off;                /* [E+1] */
+  uint32_t *part;               /* [nnz] */
+  uint32_t *count;              /* [nnz] >= 1 */
+} hgp_pins;
+
+/* f3: the pins matrix of part on level g (inbound = 0: all pins; 1: dst pins only). */
+HGP_API hgp_status hgp_pins_matrix(hgp_ctx *ctx, const hgp_csr *g, const uint32_t *part, uint32_t nparts,
+                                   int inbound, hgp_pins *out);
+HGP_API void hgp_pins_free(hgp_ctx *ctx, hgp_pins *pm);
+
+/* f1: Eq.1, Eq.16 and the loads of part (e.g. rho of hgp_coarsen on level 0).
+ * part_size / part_inbound: DEVICE u64 [nparts] receiving every partition's loads, or NULL. */
+HGP_API hgp_status hgp_partition_metrics(hgp_ctx *ctx, const hgp_csr *g, const uint32_t *part, uint32_t nparts,
+                                         uint64_t omega, uint64_t delta, hgp_quality *out, uint64_t *part_size,
+                                         uint64_t *part_inbound);
+
+/* f3: Eq.13: saving(n) = sum of omega(e) over e in I(n) with
+ * pins(rho(n), e) = 1; loss(n, p) = sum of omega(e) over e in I(n) with pins(p, e) = 0;
+ * dest[n] = the p != rho(n) holding a pin of some e in I(n) with the largest (gain(n, p), p),
+ * restricted to size(n) + |p| <= omega when enforce_size; HGP_NONE (gain 0) if none.
+ * pins: the full matrix from hgp_pins_matrix(part, inbound = 0), or NULL (computed here).
+ * dest: DEVICE u32 [N]; gain: DEVICE i64 [N]. */
+HGP_API hgp_status hgp_propose_moves(hgp_ctx *ctx, const hgp_csr *g, const uint32_t *part, uint32_t nparts,
+                                     const hgp_pins *pins, uint64_t omega, int enforce_size, uint32_t *dest,
+                                     int64_t *gain);
+
+/* f3: in-sequence gains (Eqs.14-15). seq: DEVICE [M] distinct node ids, each with
+ * dest[n] < nparts and != part[n] (else HGP_E_ARG naming the lowest bad position); gain_seq[i]
+ * (DEVICE i64 [M]) = Eq.1 before move i minus Eq.1 after it, moves 0..i-1 applied.
+ * pins: full matrix of part, or NULL. */
+HGP_API hgp_status hgp_in_sequence_gains(hgp_ctx *ctx, const hgp_csr *g, const uint32_t *part, uint32_t nparts,
+                                         const hgp_pins *pins, const uint32_t *seq, uint32_t M,
+                                         const uint32_t *dest, int64_t *gain_seq);
+
+/* f4: event-based constraint checks: violations[i] (DEVICE u32 [M]) = number of
+ * partitions with size > omega or mu-weighted inbound load > delta after moves 0..i.
+ * pins_in: the inbound matrix of part (hgp_pins_matrix(inbound = 1)), or NULL. */
+HGP_API hgp_status hgp_sequence_violations(hgp_ctx *ctx, const hgp_csr *g, const uint32_t *part, uint32_t nparts,
+                                           const hgp_pins *pins_in, const uint32_t *seq, uint32_t M,
+                                           const uint32_t *dest, uint64_t omega, uint64_t delta,
+                                           uint32_t *violations);
+
+/* f4: the landing point: *k (HOST) = the prefix length 1..M with violations[k-1]
+ * = 0 and the largest cumulative in-sequence gain *best (HOST), the shortest on ties; k = 0 and
+ * best = 0 when no such prefix has a gain > 0. gain_seq, violations: DEVICE [M]. */
+HGP_API hgp_status hgp_best_prefix(hgp_ctx *ctx, const int64_t *gain_seq, const uint32_t *violations, uint32_t M,
+                                   uint32_t *k, int64_t *best);
+
 HGP_API void hgp_csr_free(hgp_ctx *ctx, hgp_csr *g);
 HGP_API void hgp_nbrs_free(hgp_ctx *ctx, hgp_nbrs *nb);
 

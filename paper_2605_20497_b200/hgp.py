@@ -76,6 +76,17 @@ class CStats(ctypes.Structure):
                 "ms": {"score": self.ms[0], "match": self.ms[1], "contract": self.ms[2], "total": self.ms[3]}}
 
 
+class CQuality(ctypes.Structure):
+    _fields_ = [("connectivity", ctypes.c_uint64), ("cut_net", ctypes.c_uint64), ("max_size", ctypes.c_uint64),
+                ("max_inbound", ctypes.c_uint64), ("size_violations", ctypes.c_uint32),
+                ("inbound_violations", ctypes.c_uint32)]
+
+
+class CPins(ctypes.Structure):
+    _fields_ = [("E", ctypes.c_uint32), ("pad_", ctypes.c_uint32), ("nnz", ctypes.c_uint64), ("off", vp),
+                ("part", vp), ("count", vp)]
+
+
 ALLOC_FN = ctypes.CFUNCTYPE(vp, vp, ctypes.c_size_t, vp)
 FREE_FN = ctypes.CFUNCTYPE(None, vp, vp, ctypes.c_size_t, vp)
 
@@ -136,6 +147,20 @@ def lib():
                                          ctypes.POINTER(CStats)]
         L.hgp_csr_free.argtypes = [vp, ctypes.POINTER(CCsr)]
         L.hgp_nbrs_free.argtypes = [vp, ctypes.POINTER(CNbrs)]
+        cp, pp = ctypes.POINTER(CCsr), ctypes.POINTER(CPins)
+        L.hgp_pins_matrix.argtypes = [vp, cp, vp, ctypes.c_uint32, ctypes.c_int, pp]
+        L.hgp_pins_free.argtypes = [vp, pp]
+        L.hgp_partition_metrics.argtypes = [vp, cp, vp, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
+                                            ctypes.POINTER(CQuality), vp, vp]
+        L.hgp_propose_moves.argtypes = [vp, cp, vp, ctypes.c_uint32, pp, ctypes.c_uint64, ctypes.c_int, vp, vp]
+        L.hgp_in_sequence_gains.argtypes = [vp, cp, vp, ctypes.c_uint32, pp, vp, ctypes.c_uint32, vp, vp]
+        L.hgp_sequence_violations.argtypes = [vp, cp, vp, ctypes.c_uint32, pp, vp, ctypes.c_uint32, vp,
+                                              ctypes.c_uint64, ctypes.c_uint64, vp]
+        L.hgp_best_prefix.argtypes = [vp, vp, vp, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32),
+                                      ctypes.POINTER(ctypes.c_int64)]
+        for f in (L.hgp_pins_matrix, L.hgp_partition_metrics, L.hgp_propose_moves, L.hgp_in_sequence_gains,
+                  L.hgp_sequence_violations, L.hgp_best_prefix):
+            f.restype = S
         for f in (L.hgp_ctx_create, L.hgp_copy, L.hgp_sync, L.hgp_build_csr, L.hgp_unique_neighbors,
                   L.hgp_score_pairs, L.hgp_match, L.hgp_contract, L.hgp_coarsen_level,
                   L.hgp_neighbors_and_scores, L.hgp_coarsen_level0):
@@ -444,3 +469,97 @@ def cand_to_numpy(cand: torch.Tensor) -> np.ndarray:
     out["pad"] = (raw[..., 0] >> 32).astype(np.uint32)
     out["score"] = raw[..., 1]
     return out
+
+
+# ---- rows after the level: f1 quality, f3 refinement gains, f4 validation --------
+
+class Pins:
+    """A pins(p, e) / pins_in(p, e) matrix owned by the library (hgp_pins_free)."""
+
+    def __init__(self, ctx: Ctx, c: CPins):
+        self.ctx, self.c = ctx, c
+
+    nnz = property(lambda s: s.c.nnz)
+
+    def tensors(self) -> dict:
+        c = self.c
+        return {"off": dev_view(c.off, c.E + 1, "u64", self), "part": dev_view(c.part, c.nnz, "u32", self),
+                "count": dev_view(c.count, c.nnz, "u32", self)}
+
+    def to_host(self) -> dict:
+        return {k: v.cpu().numpy() for k, v in self.tensors().items()}
+
+    def free(self):
+        if self.c is not None and self.ctx.h:
+            lib().hgp_pins_free(self.ctx.h, ctypes.byref(self.c))
+        self.c = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _pins_ref(pins: "Pins | None"):
+    return ctypes.byref(pins.c) if pins is not None else None
+
+
+def pins_matrix(ctx: Ctx, g: Csr, part: torch.Tensor, nparts: int, inbound: bool = False) -> Pins:
+    """f3: sparse pins(p, e) (inbound=False) or pins_in(p, e) (inbound=True) of part (u32 device)."""
+    out = CPins()
+    _check(lib().hgp_pins_matrix(ctx.h, ctypes.byref(g.c), _ptr(part), nparts, int(inbound), ctypes.byref(out)))
+    return Pins(ctx, out)
+
+
+def partition_metrics(ctx: Ctx, g: Csr, part: torch.Tensor, nparts: int, omega: int = UNBOUNDED,
+                      delta: int = UNBOUNDED, loads: bool = False):
+    """f1: Eq.1 connectivity, Eq.16 cut-net, max loads and violation counts of part. With
+    loads=True also returns (size [nparts], inbound [nparts]) u64 device tensors."""
+    q = CQuality()
+    size = inb = None
+    if loads:
+        size = torch.empty(max(nparts, 1), dtype=torch.uint64, device="cuda")
+        inb = torch.empty(max(nparts, 1), dtype=torch.uint64, device="cuda")
+    _check(lib().hgp_partition_metrics(ctx.h, ctypes.byref(g.c), _ptr(part), nparts, omega, delta, ctypes.byref(q),
+                                       _ptr(size), _ptr(inb)))
+    d = {k: int(getattr(q, k)) for k, _ in CQuality._fields_}
+    return (d, size, inb) if loads else d
+
+
+def propose_moves(ctx: Ctx, g: Csr, part: torch.Tensor, nparts: int, omega: int = UNBOUNDED,
+                  enforce_size: bool = False, pins: Pins | None = None):
+    """f3: Eq.13 proposals -> (dest u32 [N] with NONE = no move, gain i64 [N]) device tensors."""
+    dest = torch.empty(max(g.N, 1), dtype=torch.uint32, device="cuda")
+    gain = torch.empty(max(g.N, 1), dtype=torch.int64, device="cuda")
+    _check(lib().hgp_propose_moves(ctx.h, ctypes.byref(g.c), _ptr(part), nparts, _pins_ref(pins), omega,
+                                   int(enforce_size), _ptr(dest), _ptr(gain)))
+    return dest[:g.N], gain[:g.N]
+
+
+def in_sequence_gains(ctx: Ctx, g: Csr, part: torch.Tensor, nparts: int, seq: torch.Tensor, dest: torch.Tensor,
+                      pins: Pins | None = None) -> torch.Tensor:
+    """f3: Eqs.14-15 in-sequence gains of the moves seq (u32 device) -> i64 [M] device tensor."""
+    M = seq.numel()
+    out = torch.empty(max(M, 1), dtype=torch.int64, device="cuda")
+    _check(lib().hgp_in_sequence_gains(ctx.h, ctypes.byref(g.c), _ptr(part), nparts, _pins_ref(pins), _ptr(seq), M,
+                                       _ptr(dest), _ptr(out)))
+    return out[:M]
+
+
+def sequence_violations(ctx: Ctx, g: Csr, part: torch.Tensor, nparts: int, seq: torch.Tensor, dest: torch.Tensor,
+                        omega: int, delta: int, pins_in: Pins | None = None) -> torch.Tensor:
+    """f4: event-based validation -> violations u32 [M] device tensor."""
+    M = seq.numel()
+    out = torch.empty(max(M, 1), dtype=torch.uint32, device="cuda")
+    _check(lib().hgp_sequence_violations(ctx.h, ctypes.byref(g.c), _ptr(part), nparts, _pins_ref(pins_in), _ptr(seq),
+                                         M, _ptr(dest), omega, delta, _ptr(out)))
+    return out[:M]
+
+
+def best_prefix(ctx: Ctx, gain_seq: torch.Tensor, violations: torch.Tensor):
+    """f4: the landing point -> (k, best cumulative gain)."""
+    k, b = ctypes.c_uint32(), ctypes.c_int64()
+    _check(lib().hgp_best_prefix(ctx.h, _ptr(gain_seq), _ptr(violations), gain_seq.numel(), ctypes.byref(k),
+                                 ctypes.byref(b)))
+    return int(k.value), int(b.value)

@@ -13,13 +13,19 @@ import bench  # noqa: E402
 
 def test_algorithmic_bytes_model():
     N, E, P, V, pi = 10 ** 6, 10 ** 6, 10 ** 8, 963651260, 4
-    # a2+a3 fused = 8P + 20E + 28N + 4V + 16 pi N (C2: the roofline's bytes per launch)
-    assert bench.algorithmic_bytes("a2+a3", N, E, P, V, pi) == 8 * P + 20 * E + 28 * N + 4 * V + 16 * pi * N == 4766605040
+    # the fused a2+a3 kernel is charged both rows (16P + 28E + 44N + 8V + 16 pi N)
+    assert bench.algorithmic_bytes("a2+a3", N, E, P, V, pi) == 16 * P + 28 * E + 44 * N + 8 * V + 16 * pi * N
     assert bench.algorithmic_bytes("a1", N, E, P, V, pi) == 12 * P + 36 * E + 24 * N
     assert bench.algorithmic_bytes("a4", N, E, P, V, pi) == 16 * pi * N + 4 * N
     Nc, Ec, Pc, Vc = 586685, 10 ** 6, 81582221, 413518770
     assert bench.algorithmic_bytes("a5", N, E, P, V, pi, Nc, Ec, Pc, Vc) == \
         16 * N + 4 * P + 20 * E + 8 * Pc + 20 * Ec + 4 * V + 4 * Vc + 28 * Nc
+
+
+def test_pin_visits():
+    import numpy as np
+    off = np.array([0, 3, 4, 104], dtype=np.uint64)          # |e| = 3, 1, 100
+    assert bench.pin_visits(off) == 3 * 2 + 0 + 100 * 99
 
 
 def test_kernel_step_attribution():

@@ -29,7 +29,7 @@ for s in "$@"; do
                 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b_ncu.log 2>&1
               python tools/launch_summary.py gpurun_out/launches.csv > gpurun_out/launches_summary.txt 2>&1; head -30 gpurun_out/launches_summary.txt ;;
     ncu) timeout 1500 ncu --set full --import-source on --clock-control none -k "regex:${NCU_K:-k_nbrscore}" \
-              --launch-skip ${NCU_SKIP:-1} -c 1 -o gpurun_out/${NCU_OUT:-prof} python tools/run_level.py --workload ${NCU_WL:-C2} --steps 1 \
+              --launch-skip ${NCU_SKIP:-1} -c 1 -o gpurun_out/${NCU_OUT:-prof} python tools/run_level.py --workload ${NCU_WL:-C2} --steps 1 $NCU_ARGS \
               > gpurun_out/ncu_${NCU_OUT:-prof}.log 2>&1; tail -3 gpurun_out/ncu_${NCU_OUT:-prof}.log
          python tools/ncu_summary.py gpurun_out/${NCU_OUT:-prof}.ncu-rep > gpurun_out/${NCU_OUT:-prof}_summary.txt 2>&1; cat gpurun_out/${NCU_OUT:-prof}_summary.txt ;;
     smoke) timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log ;;
