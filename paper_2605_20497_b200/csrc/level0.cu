@@ -38,111 +38,154 @@ struct FusedJob {
   const uint2 *wmu;                       // [N] (size, in_mu) packed for the validity test
 };
 
-// Phase 2b + 3 of k_nbrscore over the node's dense slot list. PACKED: every score of the node is
-// < 2^32 (S1 + cap < 2^32), so (score, id) is one u64 key and every sum and compare of the
-// validity test fits 32-bit arithmetic: sizes sum to < 2^32 (reading #2), |in(n) ∪ in(m)| <= E.
-template <int PIMAX, int THREADS, bool PACKED>
-__device__ __forceinline__ void eval_top(const ScoreJob &J, const FusedJob &F, uint32_t n, uint32_t count,
-                                         const uint32_t *keys, const uint32_t *acc, const uint16_t *ulist, uint64_t g,
-                                         uint32_t ib, uint64_t base, uint64_t *s_tops, uint32_t *s_topi) {
+// The validity test of Eq.6 on one (key, acc) pair of the dense list; writes the
+// N(n) entry (purge flag on invalid neighbours) and returns the shared-edge count and
+// the neighbour. Every sum fits 32 bits: sizes sum to < 2^32 (reading #2), |in(n) ∪ in(m)| <= E.
+struct EvalCtx {
+  uint32_t wn, inn, imask, om32, de32, ib;
+};
+__device__ __forceinline__ EvalCtx eval_ctx(const ScoreJob &J, uint32_t n, uint32_t ib) {
+  EvalCtx e;
+  e.wn = J.node_w[n];
+  e.inn = J.in_mu[n];
+  e.ib = ib;
+  e.imask = ib ? (uint32_t)((1ull << ib) - 1) : 0u;
+  e.om32 = J.omega >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)J.omega;
+  e.de32 = J.delta >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)J.delta;   // HGP_UNBOUNDED too
+  return e;
+}
+__device__ __forceinline__ bool eval_one(const FusedJob &F, const EvalCtx &E, uint2 d, uint64_t pos, uint32_t &cnt) {
+  const uint32_t v = d.x, x = d.y;
+  cnt = E.ib < 32 ? x >> E.ib : 0u;
+  const uint32_t inter = x & E.imask;
+  const uint2 wm = __ldg(F.wmu + v);                               // (size(m), in_mu(m)): one gather
+  // |in(n) ∪ in(m)| = in_mu(n) + in_mu(m) - inter; inter <= in_mu(m)
+  const bool ok = E.wn + wm.x <= E.om32 && E.inn + (wm.y - inter) <= E.de32;
+  F.pool[pos] = ok ? v : (v | kPurge);
+  return ok;
+}
+
+// Phase 3 of k_nbrscore, PACKED: every score of the node is < 2^32 (S1 + cap < 2^32), so
+// (score << 32 | id) is one u64 key ordering (score desc, id desc) exactly (Eq.6's max_id).
+// Each warp takes chunks of 4 entries per lane; per chunk, pi rounds of a warp argmax (two 32-bit
+// REDUX: the score word, then the id among its holders) over the chunk's keys and the warp's
+// running list (carried by lanes 0..pi-1) rebuild that list. Warp 0 then merges the NW lists.
+template <int PIMAX, int THREADS>
+__device__ __forceinline__ void eval_packed(const ScoreJob &J, const FusedJob &F, uint32_t n, uint32_t count,
+                                            const uint2 *dense, uint32_t g32, uint32_t ib, uint64_t base,
+                                            uint64_t *s_tops) {
   constexpr uint32_t NW = THREADS / 32;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  Top<PIMAX> top;
-  TopK<PIMAX> topk;
+  const EvalCtx E = eval_ctx(J, n, ib);
+  const uint32_t cap32 = (uint32_t)J.noise_cap;
+  uint64_t carry = 0;                                              // lane r < pi: the warp's r-th best
+  for (uint32_t c0 = w * 32; c0 < count; c0 += 4 * THREADS) {     // warp-uniform
+    uint64_t k[4];
 #pragma unroll
-  for (int i = 0; i < PIMAX; ++i) { top.s[i] = 0; top.id[i] = 0; topk.k[i] = 0; }
-  uint64_t thr = 0;                                                // topk.k[pi - 1]
-  const uint32_t wn = J.node_w[n];
-  const uint32_t inn = J.in_mu[n];
-  const uint32_t imask = ib ? (uint32_t)((1ull << ib) - 1) : 0u;
-  const uint32_t om32 = J.omega >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)J.omega;
-  const uint32_t de32 = J.delta >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)J.delta;   // HGP_UNBOUNDED too
-  const uint32_t g32 = (uint32_t)g, cap32 = (uint32_t)J.noise_cap;                  // PACKED only
-  auto visit = [&](uint32_t i, uint32_t &e_nm, uint32_t &v, bool &ok, uint64_t &sc64) {
-    const uint32_t slot = ulist[i];
-    v = keys[slot];
-    const uint32_t x = acc[slot];
-    const uint32_t cnt = ib < 32 ? x >> ib : 0u;
-    const uint32_t inter = x & imask;
-    const uint2 wm = __ldg(F.wmu + v);                             // (size(m), in_mu(m)): one gather
-    // |in(n) ∪ in(m)| = in_mu(n) + in_mu(m) - inter; inter <= in_mu(m)
-    ok = wn + wm.x <= om32 && inn + (wm.y - inter) <= de32;
-    F.pool[base + i] = ok ? v : (v | kPurge);
-    e_nm = cnt * g32;                                              // PACKED: eta(n,m) < 2^32
-    sc64 = (uint64_t)cnt * g;
-  };
-  for (uint32_t i = tid; i < count; i += THREADS) {
-    uint32_t e_nm, v; bool ok; uint64_t sc;
-    visit(i, e_nm, v, ok, sc);
-    if (!ok) continue;
-    if (PACKED) {
-      // even the largest noise cannot lift (score, id) above the current pi-th best
-      if ((((uint64_t)(e_nm + cap32) << 32) | v) <= thr) continue;
-      uint32_t s32 = e_nm;
-      if (cap32) {
-        const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
-        s32 += (uint32_t)__umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);   // uniform in [0, cap]
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = c0 + u * THREADS + lane;
+      k[u] = 0;
+      if (i < count) {
+        const uint2 d = dense[i];
+        uint32_t cnt;
+        if (eval_one(F, E, d, base + i, cnt)) {
+          uint32_t s32 = cnt * g32;                                // eta(n, m) < 2^32
+          if (cap32) {
+            const uint64_t key = ((uint64_t)min(n, d.x) << 32) | max(n, d.x);
+            s32 += (uint32_t)__umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);   // uniform in [0, cap]
+          }
+          k[u] = ((uint64_t)s32 << 32) | d.x;
+        }
       }
-      const uint64_t key = ((uint64_t)s32 << 32) | v;
-      if (key > thr) {
-        topk_insert<PIMAX>(topk, J.pi, key);
-#pragma unroll
-        for (int q = 0; q < PIMAX; ++q)
-          if (q == (int)J.pi - 1) thr = topk.k[q];
-      }
-    } else {
-      if (J.noise_cap) {
-        const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
-        sc += __umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);
-      }
-      top_insert<PIMAX>(top, J.pi, sc, v);
     }
+    uint64_t nc = 0;
+    for (uint32_t r = 0; r < J.pi; ++r) {
+      uint64_t lm = carry;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) lm = k[u] > lm ? k[u] : lm;
+      const uint32_t hi = (uint32_t)(lm >> 32);
+      const uint32_t mhi = __reduce_max_sync(0xFFFFFFFFu, hi);
+      if (mhi == 0) break;                                         // every score >= 1: nothing left
+      const uint32_t mlo = __reduce_max_sync(0xFFFFFFFFu, hi == mhi ? (uint32_t)lm : 0u);
+      const uint64_t K = ((uint64_t)mhi << 32) | mlo;              // ids are distinct: one holder
+      if (carry == K) carry = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k[u] == K) k[u] = 0;
+      if (lane == r) nc = K;
+    }
+    carry = nc;
   }
-  if (PACKED) warp_topk_merge<PIMAX>(topk, J.pi, s_tops + w * PIMAX);
-  else warp_top_merge<PIMAX>(top, J.pi, s_tops + w * PIMAX, s_topi + w * PIMAX);
+  if (lane < J.pi) s_tops[w * PIMAX + lane] = carry;
   __syncthreads();
   if (w == 0) {
-    if (PACKED) {
-      TopK<PIMAX> t2;
+    TopK<PIMAX> t2;
 #pragma unroll
-      for (int i = 0; i < PIMAX; ++i) t2.k[i] = 0;
-      for (uint32_t i = lane; i < NW * J.pi; i += 32) topk_insert<PIMAX>(t2, J.pi, s_tops[(i / J.pi) * PIMAX + i % J.pi]);
-      warp_topk_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX);
-      __syncwarp();
-      for (uint32_t r = lane; r < J.pi; r += 32) {
-        const uint64_t k = s_tops[NW * PIMAX + r];
-        hgp_cand cd;
-        cd.score = k >> 32;
-        cd.id = k ? (uint32_t)k : kNone;
-        cd.pad = 0;
-        J.cand[(uint64_t)n * J.pi + r] = cd;
-      }
-    } else {
-      Top<PIMAX> t2;
-#pragma unroll
-      for (int i = 0; i < PIMAX; ++i) { t2.s[i] = 0; t2.id[i] = 0; }
-      for (uint32_t i = lane; i < NW * J.pi; i += 32) {
-        const uint32_t ww = i / J.pi, r = i % J.pi;
-        top_insert<PIMAX>(t2, J.pi, s_tops[ww * PIMAX + r], s_topi[ww * PIMAX + r]);
-      }
-      warp_top_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX, s_topi + NW * PIMAX);
-      __syncwarp();
-      for (uint32_t r = lane; r < J.pi; r += 32) {
-        hgp_cand cd;
-        cd.score = s_tops[NW * PIMAX + r];
-        cd.id = cd.score ? s_topi[NW * PIMAX + r] : kNone;
-        cd.pad = 0;
-        J.cand[(uint64_t)n * J.pi + r] = cd;
-      }
+    for (int i = 0; i < PIMAX; ++i) t2.k[i] = 0;
+    for (uint32_t i = lane; i < NW * J.pi; i += 32) topk_insert<PIMAX>(t2, J.pi, s_tops[(i / J.pi) * PIMAX + i % J.pi]);
+    warp_topk_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX);
+    __syncwarp();
+    for (uint32_t r = lane; r < J.pi; r += 32) {
+      const uint64_t kk = s_tops[NW * PIMAX + r];
+      hgp_cand cd;
+      cd.score = kk >> 32;
+      cd.id = kk ? (uint32_t)kk : kNone;
+      cd.pad = 0;
+      J.cand[(uint64_t)n * J.pi + r] = cd;
     }
   }
 }
 
-// Shared-memory layout of k_nbrscore: keys[S] | acc[S] | dense slot list u16[S/2] | rows of the
-// current tile of incident edges: uint4 {flat end, pins index - flat start (mod 2^32), flat start
-// of dst(e), add of a src pin} and u32 {add of a dst pin}.
+// Phase 3, general: scores up to 2^62 as (u64 score, id) lists per thread, merged per warp and
+// by warp 0.
+template <int PIMAX, int THREADS>
+__device__ __forceinline__ void eval_top(const ScoreJob &J, const FusedJob &F, uint32_t n, uint32_t count,
+                                         const uint2 *dense, uint64_t g, uint32_t ib, uint64_t base, uint64_t *s_tops,
+                                         uint32_t *s_topi) {
+  constexpr uint32_t NW = THREADS / 32;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const EvalCtx E = eval_ctx(J, n, ib);
+  Top<PIMAX> top;
+#pragma unroll
+  for (int i = 0; i < PIMAX; ++i) { top.s[i] = 0; top.id[i] = 0; }
+  for (uint32_t i = tid; i < count; i += THREADS) {
+    const uint2 d = dense[i];
+    uint32_t cnt;
+    if (!eval_one(F, E, d, base + i, cnt)) continue;
+    uint64_t sc = (uint64_t)cnt * g;
+    if (J.noise_cap) {
+      const uint64_t key = ((uint64_t)min(n, d.x) << 32) | max(n, d.x);
+      sc += __umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);
+    }
+    top_insert<PIMAX>(top, J.pi, sc, d.x);
+  }
+  warp_top_merge<PIMAX>(top, J.pi, s_tops + w * PIMAX, s_topi + w * PIMAX);
+  __syncthreads();
+  if (w == 0) {
+    Top<PIMAX> t2;
+#pragma unroll
+    for (int i = 0; i < PIMAX; ++i) { t2.s[i] = 0; t2.id[i] = 0; }
+    for (uint32_t i = lane; i < NW * J.pi; i += 32) {
+      const uint32_t ww = i / J.pi, r = i % J.pi;
+      top_insert<PIMAX>(t2, J.pi, s_tops[ww * PIMAX + r], s_topi[ww * PIMAX + r]);
+    }
+    warp_top_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX, s_topi + NW * PIMAX);
+    __syncwarp();
+    for (uint32_t r = lane; r < J.pi; r += 32) {
+      hgp_cand cd;
+      cd.score = s_tops[NW * PIMAX + r];
+      cd.id = cd.score ? s_topi[NW * PIMAX + r] : kNone;
+      cd.pad = 0;
+      J.cand[(uint64_t)n * J.pi + r] = cd;
+    }
+  }
+}
+
+// Shared-memory layout of k_nbrscore: keys[S] | acc[S] | dense (key, acc) pairs uint2[S/2] | rows
+// of the current tile of incident edges: uint4 {flat end, pins index - flat start (mod 2^32),
+// flat start of dst(e), add of a src pin} and u32 {add of a dst pin}.
 constexpr uint32_t kKT = 128;     // incident edges per tile
-constexpr uint32_t fused_smem(uint32_t lg) { return (9u << lg) + kKT * 20u; }
+constexpr uint32_t fused_smem(uint32_t lg) { return (12u << lg) + kKT * 20u; }
 
 // predicated shared CAS: lanes with p == false return `dflt` without touching memory
 __device__ __forceinline__ uint32_t cas_u32_if(bool p, uint32_t a, uint32_t cmp, uint32_t val, uint32_t dflt) {
@@ -185,15 +228,15 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
   __shared__ uint32_t s_topi[(NW + 1) * PIMAX];
   __shared__ uint64_t s_sum[NW], s_g[NW];
   __shared__ uint32_t s_wsum[NW];
-  __shared__ uint32_t s_full, s_self, s_defer;
+  __shared__ uint32_t s_full, s_defer;
   __shared__ unsigned long long s_start;
   const ScoreJob &J = F.S;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   constexpr uint32_t S = 1u << LOG2S, ucap = S / 2, hmask = S - 1;
   uint32_t *keys = reinterpret_cast<uint32_t *>(dyn);
   uint32_t *acc = keys + S;
-  uint16_t *ulist = reinterpret_cast<uint16_t *>(acc + S);
-  uint4 *rows = reinterpret_cast<uint4 *>(ulist + S / 2);
+  uint2 *dense = reinterpret_cast<uint2 *>(acc + S);
+  uint4 *rows = reinterpret_cast<uint4 *>(dense + S / 2);
   uint32_t *rowd = reinterpret_cast<uint32_t *>(rows + kKT);
   // shared-window addresses kept in registers (no rematerialisation inside the pin loop)
   const uint32_t keys_s = opaque_u32(smem_u32addr(keys)), acc_s = keys_s + 4 * S;
@@ -225,8 +268,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
     bool diff = mine && tce != c0;
 #pragma unroll 1
     for (uint64_t k = i0 + kKT + tid; k < i1; k += THREADS) diff |= F.cv[J.inc[k]] != c0;
-    const uint32_t tincl = warp_incl_scan(tlen);                   // tile-0 scan of |e|
-    if (lane == 31) s_wsum[w] = tincl;
+    // tile-0 scan of |e|; does every row of the tile have >= 32 pins (then a lane's next flat
+    // position, 32 further on, is at most one row end away)?
+    // (bit 31 of a warp's published sum: one of its rows is short; sums stay < 2^29 + 2^24)
+    const uint32_t tincl = warp_incl_scan(tlen);
+    const bool tshort = __any_sync(0xFFFFFFFFu, mine && tlen < 32);
+    if (lane == 31) s_wsum[w] = tincl | (tshort ? 0x80000000u : 0u);
     const bool nonuni = __syncthreads_or(diff) != 0;               // B1 (also: the table is clean)
     uint64_t g, S1g;                                               // gcd of c(e), S1 / g
     bool small;                                                    // S1 + cap < 2^32
@@ -267,10 +314,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       if (tid == 0) F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
       continue;                                                    // nothing was inserted
     }
-    if (tid == 0) {
-      bool ins = false;
-      s_self = hs_insert_slot(keys, LOG2S, n, &ins);               // self-visits land in n's slot
-    }
+    if (tid == 0) keys[hash_slot(n, LOG2S)] = n;                  // the table is clean: n's home; self-visits land there
     // ---- phase 1, tile by tile
     bool full = false;
     for (uint64_t t0 = i0; t0 < i1; t0 += kKT) {
@@ -288,12 +332,18 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
           mu = t0 + tid < iin ? J.edge_mu[e] : 0u;
         }
         incl = warp_incl_scan(len);
-        if (lane == 31) s_wsum[w] = incl;
+        const bool sh = __any_sync(0xFFFFFFFFu, tid < kt && len < 32);
+        if (lane == 31) s_wsum[w] = incl | (sh ? 0x80000000u : 0u);
         __syncthreads();
       }
-      uint32_t woff = 0, tot = 0;
+      uint32_t woff = 0, tot = 0, anyshort = 0;
 #pragma unroll
-      for (uint32_t q = 0; q < NW; ++q) { const uint32_t x = s_wsum[q]; woff += q < w ? x : 0u; tot += x; }
+      for (uint32_t q = 0; q < NW; ++q) {
+        const uint32_t x = s_wsum[q] & 0x7FFFFFFFu;
+        anyshort |= s_wsum[q] >> 31;
+        woff += q < w ? x : 0u; tot += x;
+      }
+      const bool longrows = anyshort == 0;
       if (tid < kt) {
         const uint32_t ex = woff + incl - len;
         const uint32_t as = (uint32_t)((nonuni && ce != g ? ce / g : 1ull) << ib);
@@ -301,36 +351,13 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
         rowd[tid] = as + mu;                                       // m in dst(e), e in in(n)
       }
       __syncthreads();                                             // B2: rows (and n's slot) visible
-      // this warp's share of the tile's flat pin sequence
-      const uint32_t flo = (uint32_t)(((uint64_t)tot * w) / NW), fhi = (uint32_t)(((uint64_t)tot * (w + 1)) / NW);
-      uint32_t k = 0;
-      {
-        const uint32_t f = flo + lane;                             // first row whose end exceeds f
-        uint32_t lo_ = 0, hi_ = kt - 1;
-        while (lo_ < hi_) {
-          const uint32_t mid = (lo_ + hi_) >> 1;
-          if (rows[mid].x > f) hi_ = mid; else lo_ = mid + 1;
-        }
-        k = lo_;
-      }
-      uint4 ra = lds_v4(rows_s + 16 * k);
-      uint32_t rd = lds_u32(rowd_s + 4 * k);
-      // one 128-pin window of this warp's range; FULL: the window lies inside [flo, fhi)
-      // one 128-pin window of this warp's range; FULL: the window lies inside [flo, fhi)
-      auto window = [&](uint32_t f0, auto full_tag) {
+      // insert-or-find 4 pins per lane in the table and add their packed terms. FULL: every lane's
+      // 4 pins are valid. Claim an empty home (CAS; a first visit); hit if the home now holds m;
+      // add the packed term (a miss adds 0 to the slot it looked at: no branch); collision-displaced
+      // keys (rare) probe on.
+      auto insert4 = [&](const uint32_t (&m)[4], const uint32_t (&add)[4], const bool (&val)[4], auto full_tag) {
         constexpr bool FULL = decltype(full_tag)::value;
-        uint32_t m[4], add[4], sl[4], kk[4], miss = 0;
-        bool val[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t f = f0 + u * 32 + lane;
-          val[u] = FULL || f < fhi;
-          if (val[u]) {
-            while (f >= ra.x) { ++k; ra = lds_v4(rows_s + 16 * k); rd = lds_u32(rowd_s + 4 * k); }   // next edge
-          }
-          m[u] = val[u] ? __ldg(J.pins + (ra.y + f)) : 0u;
-          add[u] = f >= ra.z ? rd : ra.w;
-        }
+        uint32_t sl[4], kk[4], miss = 0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           sl[u] = hash_slot(m[u], LOG2S);
@@ -397,70 +424,129 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
           }
         }
       };
+      // this warp's share of the tile's flat pin sequence
+      const uint32_t flo = (uint32_t)(((uint64_t)tot * w) / NW), fhi = (uint32_t)(((uint64_t)tot * (w + 1)) / NW);
+      uint32_t k = 0;
+      {
+        const uint32_t f = flo + lane;                             // first row whose end exceeds f
+        uint32_t lo_ = 0, hi_ = kt - 1;
+        while (lo_ < hi_) {
+          const uint32_t mid = (lo_ + hi_) >> 1;
+          if (rows[mid].x > f) hi_ = mid; else lo_ = mid + 1;
+        }
+        k = lo_;
+      }
+      uint4 ra = lds_v4(rows_s + 16 * k);
+      uint32_t rd = lds_u32(rowd_s + 4 * k);
+      // one 128-pin window of this warp's flat range; FULL: the window lies inside [flo, fhi)
+      auto window = [&](uint32_t f0, auto full_tag, auto long_tag) {
+        constexpr bool FULL = decltype(full_tag)::value, LONG = decltype(long_tag)::value;
+        uint32_t m[4], add[4];
+        bool val[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t f = f0 + u * 32 + lane;
+          val[u] = FULL || f < fhi;
+          if (LONG) {
+            // every row has >= 32 pins: at most one row end lies between f - 32 and f, so a
+            // predicated single-row advance replaces the loop (no branch); the first position
+            // of the warp's range was placed by the binary search
+            const uint32_t lim = FULL ? 0xFFFFFFFFu : fhi;
+            asm volatile(
+                "{\n .reg .pred pa;\n .reg .b32 ad;\n"
+                " setp.ge.u32 pa, %7, %0;\n"
+                " setp.lt.and.u32 pa, %7, %9, pa;\n"
+                " @pa add.u32 %4, %4, 1;\n"
+                " @pa mad.lo.u32 ad, %4, 16, %6;\n"
+                " @pa ld.shared.v4.u32 {%0, %1, %2, %3}, [ad];\n"
+                " @pa mad.lo.u32 ad, %4, 4, %8;\n"
+                " @pa ld.shared.u32 %5, [ad];\n}"
+                : "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w), "+r"(k), "+r"(rd)
+                : "r"(rows_s), "r"(f), "r"(rowd_s), "r"(lim)
+                : "memory");
+          } else if (val[u]) {
+            while (f >= ra.x) { ++k; ra = lds_v4(rows_s + 16 * k); rd = lds_u32(rowd_s + 4 * k); }   // next edge(s)
+          }
+          m[u] = val[u] ? __ldg(J.pins + (ra.y + f)) : 0u;
+          add[u] = f >= ra.z ? rd : ra.w;
+        }
+        insert4(m, add, val, full_tag);
+      };
       uint32_t f0 = flo;
-      for (; f0 + 128 <= fhi; f0 += 128) window(f0, std::true_type{});
-      if (f0 < fhi) window(f0, std::false_type{});
+      if (longrows) {
+        for (; f0 + 128 <= fhi; f0 += 128) window(f0, std::true_type{}, std::true_type{});
+        if (f0 < fhi) window(f0, std::false_type{}, std::true_type{});
+      } else {
+        for (; f0 + 128 <= fhi; f0 += 128) window(f0, std::true_type{}, std::false_type{});
+        if (f0 < fhi) window(f0, std::false_type{}, std::false_type{});
+      }
       if (full) s_full = 1;
       __syncthreads();                                             // B3: rows are rewritten next
       if (s_full) break;
     }
-    if (deg == 0) __syncthreads();                                 // no tile barrier orders s_self
-    // ---- phase 2a: dense list of the occupied slots (but n's) by a ballot sweep; warp w owns the
-    //      slots [w S/NW, (w+1) S/NW): pass 1 counts, pass 2 (after the block's counts) writes
+    if (deg == 0) __syncthreads();                                 // no tile barrier orders n's own key
+    // ---- phase 2a: count the occupied slots but n's own; warp w owns the slots [w S/NW, (w+1) S/NW),
+    //      read 4 per lane (LDS.128)
     constexpr uint32_t SW = S / NW;
-    const uint32_t self = s_self, wbase = w * SW;
-    uint32_t wc = 0;
-    for (uint32_t j = 0; j < SW; j += 32) {
-      const uint32_t slot = wbase + j + lane;
-      wc += __popc(__ballot_sync(0xFFFFFFFFu, keys[slot] != kEmpty && slot != self));
+    static_assert(SW % 128 == 0, "4 slots per lane per sweep step");
+    const uint32_t wbase = w * SW;
+    uint32_t c1 = 0;
+#pragma unroll 2
+    for (uint32_t j = 4 * lane; j < SW; j += 128) {
+      const uint4 k4 = lds_v4(keys_s + 4 * (wbase + j));
+      c1 += (uint32_t)(k4.x != kEmpty && k4.x != n) + (uint32_t)(k4.y != kEmpty && k4.y != n) +
+            (uint32_t)(k4.z != kEmpty && k4.z != n) + (uint32_t)(k4.w != kEmpty && k4.w != n);
     }
+    const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c1);
     if (lane == 0) s_wsum[w] = wc;
     __syncthreads();                                               // B3'
     uint32_t woff = 0, count = 0;
 #pragma unroll
     for (uint32_t q = 0; q < NW; ++q) { const uint32_t x = s_wsum[q]; woff += q < w ? x : 0u; count += x; }
-    if (s_full || count > ucap) {                                  // table too small: next tier
-      __syncthreads();                                             // every thread has read s_full / s_wsum
-      if (tid == 0) { F.defer_list[atomicAdd(F.defer_count, 1u)] = n; s_full = 0; }
-      for (uint32_t i = tid; i < S / 4; i += THREADS) {
-        reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-        reinterpret_cast<uint4 *>(acc)[i] = make_uint4(0, 0, 0, 0);
-      }
-      continue;                                                    // B1 of the next node orders the clear
-    }
-    // ---- phase 2b: pool space for N(n) (thread 0) while the warps write the dense list
+    const bool over = s_full || count > ucap;                      // table too small: next tier
+    // ---- phase 2b: pool space for N(n) (thread 0); the warps move the occupied (key, acc) pairs
+    //      to the dense array and clear the table behind them (it is clean for the next node)
     if (tid == 0) {
       s_defer = 0;
-      const unsigned long long st = atomicAdd(F.pool_cursor, (unsigned long long)count);
-      s_start = st;
-      F.cnt[n - J.lo] = count;
-      if (st + count > F.pool_cap) {
-        s_defer = 1;
-        F.pool_list[atomicAdd(F.pool_count, 1u)] = n;
+      if (over) {
+        F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
       } else {
-        F.start[n - J.lo] = st + F.start_bias;
+        const unsigned long long st = atomicAdd(F.pool_cursor, (unsigned long long)count);
+        s_start = st;
+        F.cnt[n - J.lo] = count;
+        if (st + count > F.pool_cap) {
+          s_defer = 1;
+          F.pool_list[atomicAdd(F.pool_count, 1u)] = n;
+        } else {
+          F.start[n - J.lo] = st + F.start_bias;
+        }
       }
     }
-    for (uint32_t j = 0; j < SW; j += 32) {
-      const uint32_t slot = wbase + j + lane;
-      const bool occ = keys[slot] != kEmpty && slot != self;
-      const uint32_t b = __ballot_sync(0xFFFFFFFFu, occ);
-      if (occ) ulist[woff + __popc(b & ((1u << lane) - 1))] = (uint16_t)slot;
-      woff += __popc(b);
+#pragma unroll 2
+    for (uint32_t j = 4 * lane; j < SW; j += 128) {
+      const uint32_t ak = keys_s + 4 * (wbase + j);
+      const uint4 k4 = lds_v4(ak);
+      const uint4 a4 = lds_v4(ak + 4 * S);
+      const bool o0 = k4.x != kEmpty && k4.x != n, o1 = k4.y != kEmpty && k4.y != n;
+      const bool o2 = k4.z != kEmpty && k4.z != n, o3 = k4.w != kEmpty && k4.w != n;
+      const uint32_t c = (uint32_t)o0 + o1 + o2 + o3;
+      const uint32_t incl = warp_incl_scan(c);
+      if (!over) {
+        uint32_t p = woff + incl - c;
+        if (o0) dense[p++] = make_uint2(k4.x, a4.x);
+        if (o1) dense[p++] = make_uint2(k4.y, a4.y);
+        if (o2) dense[p++] = make_uint2(k4.z, a4.z);
+        if (o3) dense[p] = make_uint2(k4.w, a4.w);
+      }
+      woff += __shfl_sync(0xFFFFFFFFu, incl, 31);
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(ak), "r"(kEmpty) : "memory");
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(ak + 4 * S), "r"(0u) : "memory");
     }
     __syncthreads();                                               // B4
     if (tid == 0) s_full = 0;
-    if (!s_defer) {
-      if (small) eval_top<PIMAX, THREADS, true>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
-      else eval_top<PIMAX, THREADS, false>(J, F, n, count, keys, acc, ulist, g, ib, s_start, s_tops, s_topi);
-    }
-    // ---- reset the used slots (eval's barrier: every warp is done reading them)
-    for (uint32_t i = tid; i < count; i += THREADS) {
-      const uint32_t sl = ulist[i];
-      keys[sl] = kEmpty;
-      acc[sl] = 0;
-    }
-    if (tid == 0) { keys[s_self] = kEmpty; acc[s_self] = 0; }
+    if (over || s_defer) continue;                                 // (the table is already clean)
+    if (small) eval_packed<PIMAX, THREADS>(J, F, n, count, dense, (uint32_t)g, ib, s_start, s_tops);
+    else eval_top<PIMAX, THREADS>(J, F, n, count, dense, g, ib, s_start, s_tops, s_topi);
   }
 }
 

@@ -30,6 +30,14 @@ __global__ void k(uint32_t *out, uint32_t seed, long long *cyc) {
     else if (MODE == 5) acc += atomicAdd(&t[a], 1u);              // atom with return
     else if (MODE == 6) { volatile uint32_t *vk = k2; uint32_t kk = vk[a]; if (kk == a) atomicAdd(&t[a], 1u); }  // key check + red
     else if (MODE == 7) { atomicAdd((unsigned long long *)&t[a & ~1u], 1ull); }  // 64-bit
+    else if (MODE == 8) acc += atomicCAS(&k2[a], 0xFFFFFFFFu, a);   // CAS that finds the key (fails)
+    else if (MODE == 9) {                                            // CAS-always insert + branch-free add
+      const uint32_t o = atomicCAS(&k2[a], 0xFFFFFFFFu, a);
+      atomicAdd(&t[a], (o == a || o == 0xFFFFFFFFu) ? 1u : 0u);
+    } else if (MODE == 10) {                                         // key LDS + branch-free add
+      const uint32_t kk = ((volatile uint32_t *)k2)[a];
+      atomicAdd(&t[a], kk == a ? 1u : 0u);
+    }
   }
   __syncthreads();
   long long c1 = clock64();
@@ -43,12 +51,14 @@ int main() {
   uint32_t *out; long long *cyc; cudaMalloc(&out, 1 << 20); cudaMalloc(&cyc, 8);
   const char *names[] = {"red.shared.add random", "LDS+STS RMW random (racy)", "LDS random", "key LDS + RMW random",
                          "red.shared.add consecutive", "atom.shared.add (ret) random", "key LDS + red random",
-                         "atom.shared.add.u64 random"};
+                         "atom.shared.add.u64 random", "atom.shared.cas (finds key) random",
+                         "cas-always + red (branch-free)", "key LDS + red (branch-free)"};
   for (int threads : {256, 512, 1024}) {
-    for (int mode = 0; mode < 8; ++mode) {
+    for (int mode = 0; mode < 11; ++mode) {
       void (*kp)(uint32_t *, uint32_t, long long *) = nullptr;
       switch (mode) { case 0: kp = k<0>; break; case 1: kp = k<1>; break; case 2: kp = k<2>; break; case 3: kp = k<3>; break;
-                      case 4: kp = k<4>; break; case 5: kp = k<5>; break; case 6: kp = k<6>; break; default: kp = k<7>; }
+                      case 4: kp = k<4>; break; case 5: kp = k<5>; break; case 6: kp = k<6>; break; case 7: kp = k<7>; break;
+                      case 8: kp = k<8>; break; case 9: kp = k<9>; break; default: kp = k<10>; }
       const int blocks = sms * (2048 / threads);
       cudaMemset(cyc, 0, 8);
       kp<<<blocks, threads>>>(out, 1, cyc);
