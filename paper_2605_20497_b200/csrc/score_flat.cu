@@ -32,6 +32,27 @@ constexpr uint32_t flat_smem() {
   return (4u << kFLog) + ((4u << kFLog) + 16) + ((2u << kFLog) + 16) + 2 * kFCap + kFT * 24u;
 }
 
+// Bins live in 2-slot buckets: a key's probe sequence starts at the even slot (hash & ~1), so a
+// lookup reads the whole bucket with one LDS.64 and finds the key there unless both slots were
+// taken by others (~1% of keys at the loads of this tier, against ~8% of keys displaced from a
+// single home slot). A bucket with an empty slot and no match proves the key absent (linear
+// probing), so purged neighbours need no probe either.
+__device__ __forceinline__ uint32_t bucket_home(uint32_t key) { return hash_slot(key, kFLog) & ~1u; }
+__device__ __forceinline__ uint32_t bucket_insert(uint32_t *keys, uint32_t key) {
+  constexpr uint32_t mask = (1u << kFLog) - 1;
+  uint32_t s = bucket_home(key);
+  volatile uint32_t *vk = keys;
+  while (true) {
+    const uint32_t k = vk[s];
+    if (k == key) return s;
+    if (k == kEmpty) {
+      const uint32_t old = atomicCAS(&keys[s], kEmpty, key);
+      if (old == kEmpty || old == key) return s;
+    }
+    s = (s + 1) & mask;
+  }
+}
+
 template <int PIMAX>
 __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const uint64_t *cv, const uint2 *wmu) {
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -48,7 +69,9 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
   uint16_t *nslot = reinterpret_cast<uint16_t *>(inter + S / 2 + 4);  // slot of N(n)[i] (kFCap)
   uint4 *rowA = reinterpret_cast<uint4 *>(nslot + kFCap);
   uint2 *rowB = reinterpret_cast<uint2 *>(rowA + kFT);
-  const uint32_t keys_s = smem_u32addr(keys), acc_s = smem_u32addr(acc), inter_s = smem_u32addr(inter);
+  const uint32_t keys_s = opaque_u32(smem_u32addr(keys)), acc_s = opaque_u32(smem_u32addr(acc));
+  const uint32_t inter_s = opaque_u32(smem_u32addr(inter));
+  const uint32_t rowA_s = opaque_u32(smem_u32addr(rowA)), rowB_s = opaque_u32(smem_u32addr(rowB));
   const uint32_t total = J.list_count ? *J.list_count : J.hi - J.lo;
   for (uint32_t i = tid; i < S; i += kFThreads) { keys[i] = kEmpty; acc[i] = 0; if (i < S / 2) inter[i] = 0; }
   if (tid < 4) { acc[S + tid] = 0; inter[S / 2 + tid] = 0; }
@@ -75,30 +98,45 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
       tce = cv[e];
       tmu = i0 + tid < iin ? J.edge_mu[e] : 0u;
     }
-    uint64_t sum = tce, gg = tce;
-    for (uint64_t k = i0 + kFT + tid; k < i1; k += kFThreads) {
-      const uint64_t ce = cv[J.inc[k]];
-      sum += ce;
-      gg = gcd64(gg, ce);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-      const uint64_t og = __shfl_xor_sync(0xFFFFFFFFu, gg, o);
-      if (og != gg) gg = gcd64(gg, og);
-    }
-    if (lane == 0) { s_sum[w] = sum; s_g[w] = gg; }
+    // Eq.6's inbound test can only fail if in_mu(n) + in_mu(m) > Delta for some m; when even the
+    // level's largest in_mu keeps it true, inter(n, m) is never needed (the test holds whatever
+    // its value) and the bins accumulate eta alone: one shared atomic per visit, no gcd.
+    const bool nointer = J.delta == HGP_UNBOUNDED ||
+                         (J.max_in_mu && (uint64_t)inn + *J.max_in_mu <= J.delta);
+    uint64_t sum = tce;
+    for (uint64_t k = i0 + kFT + tid; k < i1; k += kFThreads) sum += cv[J.inc[k]];
+    sum = warp_sum(sum);
+    if (lane == 0) s_sum[w] = sum;
     __syncthreads();   // also: the table is clean
-    uint64_t S1 = 0, g = 0;
+    uint64_t S1 = 0, g = 1;
 #pragma unroll
-    for (uint32_t q = 0; q < NW; ++q) {
-      S1 += s_sum[q];
-      const uint64_t x = s_g[q];
-      if (x != g) g = gcd64(g, x);
+    for (uint32_t q = 0; q < NW; ++q) S1 += s_sum[q];
+    uint32_t ib = 0;
+    bool packed;
+    if (nointer && S1 < (1ull << 32)) {
+      packed = true;                                                 // acc = eta itself
+    } else {
+      // gcd of c(e) over I(n): (eta / g) << ib | inter fits 32 bits more often
+      uint64_t gg = tce;
+      for (uint64_t k = i0 + kFT + tid; k < i1; k += kFThreads) gg = gcd64(gg, cv[J.inc[k]]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t og = __shfl_xor_sync(0xFFFFFFFFu, gg, o);
+        if (og != gg) gg = gcd64(gg, og);
+      }
+      if (lane == 0) s_g[w] = gg;
+      __syncthreads();
+      g = 0;
+#pragma unroll
+      for (uint32_t q = 0; q < NW; ++q) {
+        const uint64_t x = s_g[q];
+        if (x != g) g = gcd64(g, x);
+      }
+      if (g == 0) g = 1;
+      ib = nointer || !inn ? 0 : 32 - __clz(inn);
+      const uint64_t q1 = S1 / g + 1;
+      packed = ib >= 32 ? false : q1 <= (1ull << (32 - ib));
     }
-    if (g == 0) g = 1;
-    uint32_t ib = inn ? 32 - __clz(inn) : 0;
-    const bool packed = (((unsigned __int128)(S1 / g + 1)) << ib) <= ((unsigned __int128)1 << 32);
     if (!packed && (S1 >= (1ull << 32) || inn >= (1u << 16))) {     // wide tier (CTA-uniform)
       if (tid == 0) J.wide_list[atomicAdd(J.wide_count, 1u)] = n;
       __syncthreads();
@@ -109,16 +147,10 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
     for (uint32_t i = tid; i < cnt; i += kFThreads) {
       const uint32_t v = J.nbr[b0 + i];
       uint32_t sl = 0xFFFFu;
-      if (!(v & kPurge)) {
-        bool ins = false;
-        sl = hs_insert_slot(keys, kFLog, v, &ins);
-      }
+      if (!(v & kPurge)) sl = bucket_insert(keys, v);
       nslot[i] = (uint16_t)sl;
     }
-    if (tid == 0) {
-      bool ins = false;
-      s_self = hs_insert_slot(keys, kFLog, n, &ins);                // self-visits land in n's slot
-    }
+    if (tid == 0) s_self = bucket_insert(keys, n);                  // self-visits land in n's slot
     // ---- phase 2, tile by tile
     for (uint64_t t0 = i0; t0 < i1; t0 += kFT) {
       const uint32_t kt = (uint32_t)min((uint64_t)kFT, i1 - t0);
@@ -126,7 +158,7 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
       uint64_t a = 0;
       if (tid < kt) {
         uint64_t ce = tce;
-        uint32_t mu = tmu;
+        uint32_t mu = nointer ? 0u : tmu;
         if (t0 == i0) {
           a = ta; len = tlen; ns = tns;
         } else {
@@ -135,7 +167,7 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
           len = (uint32_t)(J.edge_off[e + 1] - a);
           ns = J.edge_nsrc[e];
           ce = cv[e];
-          mu = t0 + tid < iin ? J.edge_mu[e] : 0u;
+          mu = !nointer && t0 + tid < iin ? J.edge_mu[e] : 0u;
         }
         if (packed) {
           as = (uint32_t)((ce == g ? 1ull : ce / g) << ib);
@@ -146,11 +178,17 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
         }
       }
       const uint32_t incl = warp_incl_scan(len);
-      if (lane == 31) s_wsum[w] = incl;
+      const bool sh = __any_sync(0xFFFFFFFFu, tid < kt && len < 32);   // bit 31: a short row
+      if (lane == 31) s_wsum[w] = incl | (sh ? 0x80000000u : 0u);
       __syncthreads();                                              // also orders phase 1's inserts
-      uint32_t woff = 0, tot = 0;
+      uint32_t woff = 0, tot = 0, anyshort = 0;
 #pragma unroll
-      for (uint32_t q = 0; q < NW; ++q) { const uint32_t x = s_wsum[q]; woff += q < w ? x : 0u; tot += x; }
+      for (uint32_t q = 0; q < NW; ++q) {
+        const uint32_t x = s_wsum[q] & 0x7FFFFFFFu;
+        anyshort |= s_wsum[q] >> 31;
+        woff += q < w ? x : 0u; tot += x;
+      }
+      const bool longrows = anyshort == 0;
       if (tid < kt) {
         const uint32_t ex = woff + incl - len;
         const uint64_t pp = reinterpret_cast<uint64_t>(J.pins + a) - 4ull * ex;   // &pins[a] - ex
@@ -171,57 +209,88 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
       }
       uint4 ra = rowA[k];
       uint2 rb = rowB[k];
-      auto window = [&](uint32_t f0, auto full_tag) {
-        constexpr bool FULL = decltype(full_tag)::value;
-        uint32_t m[4], add[4], iad[4], sl[4], kk[4];
+      auto window = [&](uint32_t f0, auto full_tag, auto long_tag, auto packed_tag) {
+        constexpr bool FULL = decltype(full_tag)::value, LONG = decltype(long_tag)::value;
+        constexpr bool PK = decltype(packed_tag)::value;   // == packed (CTA-uniform)
+        uint32_t m[4], add[4], iad[4], sl[4];
         bool val[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t f = f0 + u * 32 + lane;
           val[u] = FULL || f < fhi;
-          if (val[u]) {
+          if (LONG) {
+            // rows of >= 32 pins: at most one row end between f - 32 and f (predicated advance)
+            const uint32_t lim = FULL ? 0xFFFFFFFFu : fhi;
+            asm volatile(
+                "{\n .reg .pred pa;\n .reg .b32 ad;\n"
+                " setp.ge.u32 pa, %7, %4;\n"
+                " setp.lt.and.u32 pa, %7, %10, pa;\n"
+                " @pa add.u32 %6, %6, 1;\n"
+                " @pa mad.lo.u32 ad, %6, 16, %8;\n"
+                " @pa ld.shared.v4.u32 {%0, %1, %2, %3}, [ad];\n"
+                " @pa mad.lo.u32 ad, %6, 8, %9;\n"
+                " @pa ld.shared.v2.u32 {%4, %5}, [ad];\n}"
+                : "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w), "+r"(rb.x), "+r"(rb.y), "+r"(k)
+                : "r"(f), "r"(rowA_s), "r"(rowB_s), "r"(lim)
+                : "memory");
+          } else if (val[u]) {
             while (f >= rb.x) { ++k; ra = rowA[k]; rb = rowB[k]; }
           }
           const uint32_t *pf = reinterpret_cast<const uint32_t *>(((uint64_t)ra.y << 32) | ra.x) + f;
           m[u] = val[u] ? __ldg(pf) : kEmpty;
           const bool dst = f >= ra.z;
-          add[u] = packed && dst ? rb.y : ra.w;                     // packed term, or split eta
-          iad[u] = !packed && dst ? rb.y : 0u;                      // split: inter += mu
+          add[u] = PK && dst ? rb.y : ra.w;                         // packed term, or split eta
+          iad[u] = !PK && dst ? rb.y : 0u;                          // split: inter += mu
         }
+        uint2 kb[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          sl[u] = hash_slot(m[u], kFLog);
-          kk[u] = lds_u32(keys_s + 4 * sl[u]);
+          sl[u] = bucket_home(m[u]);
+          asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(kb[u].x), "=r"(kb[u].y) : "r"(keys_s + 4 * sl[u]));
         }
         bool anym = false;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const bool hit = val[u] && kk[u] == m[u];
-          if (hit) {
-            red_add_u32(acc_s + 4 * sl[u], add[u]);
-            if (iad[u]) red_add_u32(inter_s + 4 * (sl[u] >> 1), iad[u] << (16 * (sl[u] & 1)));
+          const bool h0 = kb[u].x == m[u], h1 = kb[u].y == m[u];
+          // hit in the bucket, or absent (an empty slot in the bucket and no match): trash slot S
+          const bool hit = h0 || h1;
+          const bool absent = !hit && (kb[u].x == kEmpty || kb[u].y == kEmpty);
+          const uint32_t slot = hit ? sl[u] + (h1 ? 1u : 0u) : S;
+          const bool done = val[u] && (hit || absent);
+          if (done) {
+            red_add_u32(acc_s + 4 * slot, add[u]);
+            if (!PK && iad[u]) red_add_u32(inter_s + 4 * (slot >> 1), iad[u] << (16 * (slot & 1)));
           }
-          val[u] = val[u] && !hit;                                   // val now marks the misses
+          val[u] = val[u] && !done;                                  // val now marks the rest
           anym |= val[u];
         }
-        if (__any_sync(0xFFFFFFFFu, anym)) {                        // displaced or absent keys
+        if (__any_sync(0xFFFFFFFFu, anym)) {                        // both bucket slots taken by others
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (!val[u]) continue;
-            uint32_t slot = sl[u], k2 = kk[u];
+            uint32_t slot = (sl[u] + 1) & hmask, k2 = kb[u].y;
             while (k2 != m[u]) {
               if (k2 == kEmpty) { slot = S; break; }                 // purged neighbour -> trash
               slot = (slot + 1) & hmask;
               k2 = lds_u32(keys_s + 4 * slot);
             }
             red_add_u32(acc_s + 4 * slot, add[u]);
-            if (iad[u]) red_add_u32(inter_s + 4 * (slot >> 1), iad[u] << (16 * (slot & 1)));
+            if (!PK && iad[u]) red_add_u32(inter_s + 4 * (slot >> 1), iad[u] << (16 * (slot & 1)));
           }
         }
       };
       uint32_t f0 = flo;
-      for (; f0 + 128 <= fhi; f0 += 128) window(f0, std::true_type{});
-      if (f0 < fhi) window(f0, std::false_type{});
+      auto windows = [&](auto packed_tag) {
+        if (longrows) {
+          for (; f0 + 128 <= fhi; f0 += 128) window(f0, std::true_type{}, std::true_type{}, packed_tag);
+          if (f0 < fhi) window(f0, std::false_type{}, std::true_type{}, packed_tag);
+        } else {
+          for (; f0 + 128 <= fhi; f0 += 128) window(f0, std::true_type{}, std::false_type{}, packed_tag);
+          if (f0 < fhi) window(f0, std::false_type{}, std::false_type{}, packed_tag);
+        }
+      };
+      if (packed) windows(std::true_type{});
+      else windows(std::false_type{});
       __syncthreads();                                              // rows are rewritten by the next tile
     }
     if (i1 == i0) __syncthreads();                                  // phase 1's inserts before phase 3
@@ -318,9 +387,15 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
   }
 }
 
-__global__ void k_pack_wmu2(const uint32_t *node_w, const uint32_t *in_mu, uint32_t N, uint2 *wmu) {
-  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
+__global__ void k_pack_wmu2(const uint32_t *node_w, const uint32_t *in_mu, uint32_t N, uint2 *wmu,
+                            unsigned int *max_in_mu) {
+  uint32_t mx = 0;
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
     wmu[n] = make_uint2(node_w[n], in_mu[n]);
+    mx = max(mx, in_mu[n]);
+  }
+  mx = warp_max(mx);
+  if (lane_id() == 0) atomicMax(max_in_mu, mx);
 }
 
 __global__ void k_edge_cv2(const uint64_t *edge_off, const uint32_t *edge_w, uint32_t E, uint32_t norm, uint64_t *cv) {
@@ -344,9 +419,11 @@ hgp_status launch_score_flat(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t E) {
   HGP_TRY(launch(c, "edge_cv", k_edge_cv2, dim3(E ? (div_up(E, 256) < 4096 ? div_up(E, 256) : 4096) : 0), dim3(256), 0,
                  J.edge_off, J.edge_w, E, J.norm, cv));
   uint2 *wmu = scratch_raw<uint2>(c, J.N ? J.N : 1, &st);
+  unsigned int *mx = scratch_zero<unsigned int>(c, 1, &st);
   if (st) return st;
   HGP_TRY(launch(c, "pack_wmu", k_pack_wmu2, dim3(J.N ? (div_up(J.N, 256) < 4096 ? div_up(J.N, 256) : 4096) : 0), dim3(256),
-                 0, J.node_w, J.in_mu, J.N, wmu));
+                 0, J.node_w, J.in_mu, J.N, wmu, mx));
+  J.max_in_mu = mx;
   const uint32_t grid = J.list ? 4u * c->sm_count : (nn < 4u * c->sm_count ? (nn ? nn : 1) : 4u * c->sm_count);
   return launch(c, "score_F", k_score_flat<PIMAX>, dim3(grid), dim3(kFThreads), flat_smem(), J, (const uint64_t *)cv,
                 (const uint2 *)wmu);
