@@ -15,10 +15,12 @@ on the level-0 hypergraph of the configured workload (default C2: SNN-mapping, 1
   cpu_baseline: the CPU oracle (oracle/, single thread) on a bounded sample of the same recipe
 
 `--impl reference` times the oracle alone (the tier's reference arm) on a bounded sample.
-Multi-GPU (torchrun, N>1): the level is sharded by node range (shard.py): every rank holds the
-replicated CSR, runs the fused a2+a3 on its equal-work node range, the candidate rows and N(n)
-segments are all-gathered with NCCL, a4 + a5 run replicated; value = P / step time (strong
-scaling; the result is bit-identical to 1 GPU).
+Multi-GPU (torchrun, N>1): the level is sharded (shard.py): every rank holds the
+replicated CSR, runs the fused a2+a3 on its equal-work node range; the candidate rows are
+all-gathered (NCCL), a4 runs replicated, a5 builds the coarse edges of the rank's edge range, the
+ranges are all-gathered and merged replicated, and each rank builds the coarse neighbours of its
+coarse node range with a halo exchange of partners' N(b). value = P / step time (strong scaling;
+bit-identical to 1 GPU). The line carries the per-phase compute / communication split.
 """
 from __future__ import annotations
 
@@ -329,6 +331,7 @@ def main():
     last = {}
 
     from paper_2605_20497_b200 import shard
+    comm = shard.DistComm() if world > 1 else None
 
     def step(inp):
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -338,10 +341,16 @@ def main():
         last["a1_events"] = (ea, eb)
         if world == 1:   # N(n) is consumed by a5 where the fused kernel left it (not returned)
             nb, cg, cnb, st = hgp.coarsen_level0(ctx, g, params, cand, match, gamma, want_nbrs=False)
-        else:   # node-range shards of a2+a3, NCCL all-gathers, replicated a4 + a5 (shard.py)
-            nb, cg, cnb, info = shard.level0_sharded(ctx, g, params, cand, match, gamma)
-            st = {"Nc": cg.N, "Ec": cg.E, "Pc": cg.P, "Vc": cnb.V, "V": nb.V, "matched_per_round": [], "purged": 0,
-                  "merged_edges": 0, "dropped_edges": 0}
+        else:   # the sharded level (shard.py): a2+a3 / a5 on this rank's ranges, NCCL exchanges
+            bounds = hgp.shard_bounds(ctx, g, world)
+            states = [shard.RankState(rank, bounds[rank], bounds[rank + 1])]
+            cg, info = shard.level_sharded(ctx, g, params, states, comm, True, cand, match, gamma)
+            cnb, nb = states[0].nb, None
+            vt = torch.tensor([info.V, cnb.V], dtype=torch.int64, device="cuda")
+            dist.all_reduce(vt)                                          # V and V' summed over the ranks
+            st = {"Nc": cg.N, "Ec": cg.E, "Pc": cg.P, "Vc": int(vt[1].item()), "V": int(vt[0].item()),
+                  "matched_per_round": [info.pairs],
+                  "purged": 0, "merged_edges": 0, "dropped_edges": 0, "phase_ms": info.ms}
         last.update(st=st, V=nb.V if nb is not None else st["V"])
         for x in (g, nb, cg, cnb):
             if x is not None:
@@ -445,6 +454,28 @@ def main():
         if not args.no_refine:
             hier_q, refine = refine_leg(hgp, ctx, hierarchy, omega, delta, stream)
             hier["initial_partition"] = hier_q
+    else:   # the sharded driver (shard.coarsen_sharded): same levels as hgp_coarsen, per-phase split
+        def hierarchy_sharded():
+            g = hgp.build_csr(ctx, N, dev["edge_off"], dev["edge_nsrc"], dev["pins"], dev["edge_w"], dev["node_w"])
+            rho, levels, cg, states = shard.coarsen_sharded(ctx, g, params, comm)
+            for x in [g, cg] + [s_.nb for s_ in states]:
+                x.free()
+            return levels, cg.N
+        hierarchy_sharded()
+        barrier()
+        t_0 = time.perf_counter()
+        levels, n_last = hierarchy_sharded()
+        torch.cuda.synchronize()
+        hms = max_over_ranks((time.perf_counter() - t_0) * 1e3)
+        phases = {}
+        for l in levels:
+            for k, v in l.ms.items():
+                phases[k] = round(phases.get(k, 0.0) + v, 3)
+        comm_ms = sum(v for k, v in phases.items() if k.startswith("X"))
+        hier = {"what": "a1 + every level to the stop rule, sharded (shard.coarsen_sharded; host wall clock, max "
+                        "over ranks)", "levels": len(levels), "total_coarsening_ms": hms, "pins_per_s": P / (hms / 1e3),
+                "coarsest_nodes": n_last, "level_nodes": [l.N for l in levels], "phase_ms_total": phases,
+                "comm_ms": round(comm_ms, 3), "compute_ms": round(sum(phases.values()) - comm_ms, 3)}
 
     if rank != 0:
         if world > 1:
@@ -495,7 +526,7 @@ def main():
         "clocks": clk,
         "roofline": roof,
         "issue_roofline": issue_roofline(dominant, args.workload, fam_ms_step, clk),
-        "level": {"Nc": st["Nc"], "Ec": st["Ec"], "Pc": st["Pc"], "Vc": st["Vc"],
+        "level": {"Nc": st["Nc"], "Ec": st["Ec"], "Pc": st["Pc"], "Vc": st["Vc"], "phase_ms": st.get("phase_ms"),
                   "matched_fraction": float((match.view(torch.int32) != -1).sum().item()) / N,
                   "matched_per_round": st["matched_per_round"], "purged": st["purged"],
                   "merged_edges": st["merged_edges"], "dropped_edges": st["dropped_edges"]},

@@ -175,6 +175,33 @@ HGP_API hgp_status hgp_profile_end(hgp_ctx *ctx, double *total_ms, uint64_t *lau
 /* After hgp_profile_end: per kernel name "name:ms:launches;" into the HOST buffer buf. */
 HGP_API hgp_status hgp_profile_report(hgp_ctx *ctx, char *buf, size_t len);
 
+/* Work counters per kernel tier (tests: every tier is exercised). Counter i counts the
+ * nodes (or node rounds) the tier processed since the ctx was created or last reset; the
+ * counting costs one atomic per CTA per launch. Indices: */
+enum {
+  HGP_TIER_FUSED_S = 0,      /* fused a2+a3, sampled first tier (every 64th node) */
+  HGP_TIER_FUSED_A = 1,      /* fused a2+a3, 4096-slot table */
+  HGP_TIER_FUSED_M = 2,      /* fused a2+a3, 8192-slot table */
+  HGP_TIER_FUSED_B = 3,      /* fused a2+a3, 16384-slot table */
+  HGP_TIER_NBRS_1 = 4,       /* a2 unfused, smem tier 1 (range and list forms) */
+  HGP_TIER_NBRS_2 = 5,       /* a2 unfused, smem tier 2 */
+  HGP_TIER_NBRS_3 = 6,       /* a2 unfused, global-memory tables */
+  HGP_TIER_SCORE_NOINTER = 7, /* a3 first tier, eta only (Delta test cannot fail) */
+  HGP_TIER_SCORE_PACKED = 8, /* a3 first tier, (eta/g) << ib | inter in one u32 */
+  HGP_TIER_SCORE_SPLIT = 9,  /* a3 first tier, u32 eta + u16 inter */
+  HGP_TIER_SCORE_B = 10,     /* a3 big neighbourhoods, packed */
+  HGP_TIER_SCORE_W = 11,     /* a3 64-bit eta, smem */
+  HGP_TIER_SCORE_H = 12,     /* a3 64-bit eta, global-memory tables */
+  HGP_TIER_CNBRS_A = 13,     /* a5 coarse neighbours, 4096-slot table */
+  HGP_TIER_CNBRS_M = 14,     /* a5 coarse neighbours, 16384-slot table */
+  HGP_TIER_CNBRS_B = 15,     /* a5 coarse neighbours, 32768-slot table */
+  HGP_TIER_CNBRS_C = 16,     /* a5 coarse neighbours, global-memory tables */
+  HGP_TIER_JUMP = 17,        /* a4 pointer-jumping fallback (nodes of over-long best-child chains) */
+  HGP_TIERS = 24
+};
+/* HOST out[HGP_TIERS] <- the counters (synchronises); reset != 0 zeroes them afterwards. */
+HGP_API hgp_status hgp_tier_counts(hgp_ctx *ctx, uint64_t *out, int reset);
+
 /* ---- the level's steps ------------------------------------------------------------------ */
 /* a1: validate the input and build the canonical level-0 CSR (mu = 1). Synchronises. */
 HGP_API hgp_status hgp_build_csr(hgp_ctx *ctx, const hgp_input *in, hgp_csr *out);
@@ -255,6 +282,55 @@ HGP_API hgp_status hgp_leftover_pairs(hgp_ctx *ctx, const hgp_cand *cand, uint32
 HGP_API hgp_status hgp_coarsen(hgp_ctx *ctx, const hgp_csr *g0, const hgp_params *p, uint32_t max_levels,
                                uint32_t *rho, hgp_csr *coarsest, hgp_nbrs *coarsest_nb, hgp_level_stats *stats,
                                uint32_t *levels_out);
+
+/* ---- a5 in pieces, for node/edge-range shards over several GPUs --------------
+ * hgp_contract is hgp_gamma + hgp_contract_edges(all edges) + hgp_contract_merge +
+ * hgp_coarse_neighbors(all coarse nodes) on one GPU. On W GPUs every rank holds the replicated
+ * fine CSR and match (a4 is replicated), builds the coarse edges of its fine edge range, the
+ * ranges' hgp_cedges are all-gathered in rank order (= ascending fine edge id; the caller's
+ * collective, e.g. NCCL through torch.distributed), the merge runs replicated, and each rank builds
+ * the coarse neighbours of the coarse nodes whose min member it owns — the partner's N(b) comes
+ * from its owner by a halo exchange (the caller's point-to-point). Results equal hgp_contract's. */
+
+/* gamma (reading #11) of a symmetric match: DEVICE gamma[N]; *Nc (HOST) = N'. */
+HGP_API hgp_status hgp_gamma(hgp_ctx *ctx, const uint32_t *match, uint32_t N, uint32_t *gamma, uint32_t *Nc);
+
+/* Coarse node ranges of node-range shards: coarse_bounds[i] (HOST) = number of coarse nodes whose
+ * min member is < node_bounds[i] (HOST [nbounds], each <= N): the coarse nodes a rank owning
+ * [b_r, b_{r+1}) builds the neighbours of are [coarse_bounds[r], coarse_bounds[r+1]). */
+HGP_API hgp_status hgp_coarse_bounds(hgp_ctx *ctx, const uint32_t *match, uint32_t N, const uint32_t *node_bounds,
+                                     uint32_t nbounds, uint32_t *coarse_bounds);
+
+/* Coarse edges of the fine edges [elo, ehi) before the parallel-edge merge: for every
+ * kept fine edge (D' != ∅ or |S'| >= 2, reading #14), ascending. Library-owned DEVICE arrays. */
+typedef struct {
+  uint32_t K, pad_;            /* kept fine edges */
+  uint64_t P;                  /* sum of their coarse sizes */
+  uint32_t *eid;               /* [K]   fine edge id, ascending */
+  uint64_t *fp;                /* [K]   64-bit fingerprint of (|S'|, S', D') (hash only; equality is verified) */
+  uint32_t *nsrc;              /* [K]   |S'| */
+  uint32_t *size;              /* [K]   |S'| + |D'| */
+  uint64_t *off;               /* [K+1] */
+  uint32_t *pins;              /* [P]   S' ascending ‖ D' ascending, per edge */
+} hgp_cedges;
+HGP_API hgp_status hgp_contract_edges(hgp_ctx *ctx, const hgp_csr *g, const uint32_t *gamma, uint32_t elo,
+                                      uint32_t ehi, hgp_cedges *out);
+HGP_API void hgp_cedges_free(hgp_ctx *ctx, hgp_cedges *ce);
+
+/* The coarse level's edges and incidence from `all` (every range's hgp_cedges concatenated in
+ * ascending fine id, offsets rebased; DEVICE arrays borrowed): identical (S', D') merged (omega' and
+ * mu' summed, ordered by the minimum fine id; reading #12); gamma (DEVICE [N]) recomputed from match;
+ * coarse node sizes. coarse is library-owned (hgp_csr_free). */
+HGP_API hgp_status hgp_contract_merge(hgp_ctx *ctx, const hgp_csr *g, const uint32_t *match, uint32_t *gamma,
+                                      const hgp_cedges *all, hgp_csr *coarse);
+
+/* Coarse neighbours (readings #7, #16) of the coarse nodes [clo, chi): for c with
+ * members a (min) and b, gamma(N(a) ∪ N(b)) minus OR-flagged entries minus c. Fine node n's N(n)
+ * is nbr[seg_start[n] .. seg_start[n] + seg_len[n]) (DEVICE [N] arrays; only members of
+ * [clo, chi) are read). out covers [clo, chi) (library-owned). */
+HGP_API hgp_status hgp_coarse_neighbors(hgp_ctx *ctx, const uint32_t *match, const uint32_t *gamma, uint32_t N,
+                                        const uint64_t *seg_start, const uint32_t *seg_len, const uint32_t *nbr,
+                                        uint32_t clo, uint32_t chi, hgp_nbrs *out);
 
 /* ---- rows after the level: f1 quality, f3 refinement gains, f4 validation ----
  * A partition is part[N] (DEVICE) with ids < nparts; any id >= nparts is HGP_E_ARG naming the

@@ -55,6 +55,8 @@ struct hgp_ctx {
   int depth = 0;
   uint64_t launches = 0;
   uint64_t *d_err = nullptr;       // [kErrSlots] device
+  unsigned long long *d_tiers = nullptr;   // [HGP_TIERS] device work counters per kernel tier
+  uint64_t h_tiers[HGP_TIERS] = {};        // host-side part (tiers the host decides, e.g. a4 jumps)
   uint64_t *h_pin = nullptr;       // [64] pinned host staging
   cudaEvent_t ev[8] = {};
   // explicit options (hgp_ctx_set_option; tests and experiments only — no environment variables)
@@ -265,6 +267,11 @@ __device__ __forceinline__ T warp_incl_scan(T v) {
     if (lane >= (uint32_t)o) v += w;
   }
   return v;
+}
+
+// Work counter of a kernel tier: thread 0 of a CTA adds the nodes it processed, once per launch.
+__device__ __forceinline__ void tier_add(unsigned long long *tiers, int tier, uint64_t n) {
+  if (tiers && n) atomicAdd(tiers + tier, (unsigned long long)n);
 }
 
 __device__ __forceinline__ void report_min(uint64_t *err, int slot, uint64_t idx) {

@@ -37,7 +37,7 @@ __global__ void k_gamma(const uint32_t *match, const uint64_t *cid, const uint32
     const uint32_t lo = (m == kNone || n < m) ? n : m;
     const uint32_t c = (uint32_t)cid[lo];
     gamma[n] = c;
-    atomicAdd(&cw[c], node_w[n]);
+    if (cw) atomicAdd(&cw[c], node_w[n]);
     if (lo == n) { mem0[c] = n; mem1[c] = m; }
   }
 }
@@ -126,12 +126,16 @@ __global__ void k_edge_unique(const uint64_t *off, const uint32_t *nsrc, uint32_
   }
 }
 
+// Entries k of the merge: the fine edge eid[k] (identity when eid == nullptr) whose coarse pins
+// are x[off[k] .. off[k] + csize[k]); keep == nullptr: every entry is kept. Entries ascend by
+// fine edge id, so the class representative (the minimum fine id) is the minimum entry.
 struct MergeJob {
   const uint64_t *off;
   const uint32_t *x, *cnsrc, *csize;
   const uint8_t *keep;
   const uint64_t *fp;
-  uint32_t E;
+  const uint32_t *eid;
+  uint32_t E;                // entries
   uint32_t *owner;     // table slots: edge id of the first inserter (kEmpty = free)
   uint32_t *minrep;    // per slot: min edge id of the class
   uint32_t *slot_of;   // per edge
@@ -149,7 +153,7 @@ __device__ __forceinline__ bool same_edge(const MergeJob &M, uint32_t a, uint32_
 __global__ void k_merge_insert(MergeJob M) {
   const uint32_t mask = (1u << M.log2t) - 1;
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < M.E; e += gridDim.x * blockDim.x) {
-    if (!M.keep[e]) continue;
+    if (M.keep && !M.keep[e]) continue;
     uint32_t slot = (uint32_t)(M.fp[e] >> 7) & mask;
     while (true) {
       uint32_t o = *(volatile uint32_t *)&M.owner[slot];
@@ -167,7 +171,7 @@ __global__ void k_merge_insert(MergeJob M) {
 
 __global__ void k_merge_resolve(MergeJob M, uint32_t *rep, uint32_t *is_rep) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < M.E; e += gridDim.x * blockDim.x) {
-    const uint32_t r = M.keep[e] ? M.minrep[M.slot_of[e]] : kNone;
+    const uint32_t r = (!M.keep || M.keep[e]) ? M.minrep[M.slot_of[e]] : kNone;
     rep[e] = r;
     is_rep[e] = r == e;
   }
@@ -175,13 +179,15 @@ __global__ void k_merge_resolve(MergeJob M, uint32_t *rep, uint32_t *is_rep) {
 
 __global__ void k_coarse_edge_attrs(const uint32_t *rep, const uint64_t *ceid, const uint32_t *edge_w,
                                     const uint32_t *edge_mu, const uint32_t *cnsrc, const uint32_t *csize, uint32_t E,
-                                    uint32_t *cw, uint32_t *cmu, uint32_t *c_nsrc, uint32_t *c_size) {
+                                    const uint32_t *eid, uint32_t *cw, uint32_t *cmu, uint32_t *c_nsrc,
+                                    uint32_t *c_size) {
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
     const uint32_t r = rep[e];
     if (r == kNone) continue;
     const uint32_t ce = (uint32_t)ceid[r];
-    atomicAdd(&cw[ce], edge_w[e]);
-    atomicAdd(&cmu[ce], edge_mu[e]);
+    const uint32_t fe = eid ? eid[e] : e;                          // the fine edge of entry e
+    atomicAdd(&cw[ce], edge_w[fe]);
+    atomicAdd(&cmu[ce], edge_mu[fe]);
     if (r == e) { c_nsrc[ce] = cnsrc[e]; c_size[ce] = csize[e]; }
   }
 }
@@ -222,6 +228,9 @@ struct CNbrJob {
   uint32_t log2s;
   uint32_t *gtab;              // global tables (keys | flags) when not in smem
   unsigned long long *purged;
+  unsigned long long *tiers;   // work counters (hgp_tier_counts)
+  int tier;
+  uint32_t cbase;              // coarse id of local coarse node 0 (a range of coarse nodes)
 };
 
 // insert key with an OR-ed flag kept in bit 31 of the slot (ids < 2^31 - 1, kEmpty masks to
@@ -261,6 +270,7 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
   const uint32_t hmask = S - 1;
   const uint32_t total = J.list_count ? *J.list_count : J.Nc;
   uint64_t purged = 0;
+  uint32_t done = 0;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t c = J.list ? J.list[t] : t;
     const uint32_t a = J.mem0[c], b = J.mem1[c];
@@ -319,7 +329,7 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
     uint32_t mine = 0;
     for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
       const uint32_t k = keys[sb + lane];
-      mine += __popc(__ballot_sync(0xFFFFFFFFu, !(k & kPurge) && k != c));   // kEmpty has bit 31 set
+      mine += __popc(__ballot_sync(0xFFFFFFFFu, !(k & kPurge) && k != c + J.cbase));   // kEmpty has bit 31 set
     }
     if (lane == 0) s_wcnt[w] = mine;
     __syncthreads();
@@ -328,14 +338,15 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
     const uint64_t base = J.bound_off[c];
     for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
       const uint32_t k = keys[sb + lane];
-      const bool keep = !(k & kPurge) && k != c;
+      const bool keep = !(k & kPurge) && k != c + J.cbase;
       const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
       if (keep) J.pool[base + wpos + __popc(bal & lt)] = k;
       wpos += __popc(bal);
     }
-    if (tid == 0) J.cnt[c] = tot;
+    if (tid == 0) { J.cnt[c] = tot; ++done; }
     __syncthreads();
   }
+  if (tid == 0) tier_add(J.tiers, J.tier, done);
   purged = warp_sum(purged);
   if ((tid & 31) == 0 && purged) atomicAdd(J.purged, (unsigned long long)purged);
 }
@@ -393,24 +404,21 @@ static constexpr uint32_t kCALog = 12, kCAThreads = 256;   // 4096 slots: 16 KB,
 static constexpr uint32_t kCMLog = 14, kCMThreads = 256;   // 16384 slots: 64 KB, <= 8192 entries (3 CTAs/SM)
 static constexpr uint32_t kCBLog = 15, kCBThreads = 256;   // 32768 slots: 128 KB, <= 16384 entries
 
-hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match, uint32_t *gamma,
-                         hgp_csr *C, hgp_nbrs *CN, hgp_level_stats *stats, const SegView *view) {
+static uint32_t grid_n(hgp_ctx *c, uint64_t n, uint32_t per = 256) {
+  const uint64_t b = (n + per - 1) / per, cap = 16ull * c->sm_count;
+  return (uint32_t)(b < cap ? (b ? b : 1) : cap);
+}
+
+// gamma (reading #11): coarse id = rank of the cluster's min member; coarse sizes;
+// members mem0 (min) / mem1 (partner or NONE) of every coarse node. mem may be nullptr.
+static hgp_status gamma_impl(hgp_ctx *c, const uint32_t *match, uint32_t N, const uint32_t *node_w, uint32_t *gamma,
+                             uint32_t *Nc_out, uint32_t **cw_out, uint32_t **mem_out, bool cw_device_owned) {
   hgp_status st = HGP_OK;
-  const uint32_t N = g->N, E = g->E;
-  const uint64_t P = g->P;
-  memset(C, 0, sizeof(*C));
-  memset(CN, 0, sizeof(*CN));
-  HGP_TRY(clear_errors(c));
-  auto grid_for = [&](uint64_t n, uint32_t per = 256) -> uint32_t {
-    uint64_t b = (n + per - 1) / per;
-    uint64_t cap = 16ull * c->sm_count;
-    return (uint32_t)(b < cap ? (b ? b : 1) : cap);
-  };
-  // ---- gamma
   uint32_t *rep = scratch_raw<uint32_t>(c, N, &st);
   uint64_t *cid = scratch_raw<uint64_t>(c, (size_t)N + 1, &st);
   if (st) return st;
-  HGP_TRY(launch(c, "rep", k_rep, dim3(grid_for(N)), dim3(256), 0, match, N, rep, c->d_err));
+  HGP_TRY(clear_errors(c));
+  HGP_TRY(launch(c, "rep", k_rep, dim3(grid_n(c, N)), dim3(256), 0, match, N, rep, c->d_err));
   uint64_t Nc64 = 0;
   HGP_TRY(scan_exclusive(c, InU32{rep}, N, cid, &Nc64));
   uint64_t err[kErrSlots];
@@ -418,45 +426,121 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   if (err[kErrMatch] != UINT64_MAX)
     return set_error(HGP_E_ARG, "node %llu: match is not symmetric", (unsigned long long)err[kErrMatch]);
   const uint32_t Nc = (uint32_t)Nc64;
-  C->N = Nc;
-  C->node_w = dalloc_n<uint32_t>(c, Nc, &st);
+  uint32_t *cw = !node_w ? nullptr : cw_device_owned ? dalloc_n<uint32_t>(c, Nc, &st) : scratch_raw<uint32_t>(c, Nc, &st);
   uint32_t *mem = scratch_raw<uint32_t>(c, 2 * (size_t)Nc, &st);
   if (st) return st;
-  uint32_t *mem0 = mem, *mem1 = mem + Nc;
-  HGP_CUDA(cudaMemsetAsync(C->node_w, 0, 4 * (size_t)(Nc ? Nc : 1), c->stream));
-  HGP_TRY(launch(c, "gamma", k_gamma, dim3(grid_for(N)), dim3(256), 0, match, (const uint64_t *)cid,
-                 (const uint32_t *)g->node_w, N, gamma, C->node_w, mem0, mem1));
-  // ---- coarse edges in oversized slots
-  uint32_t *x = scratch_raw<uint32_t>(c, P, &st);
-  uint32_t *cnsrc = scratch_raw<uint32_t>(c, E, &st);
-  uint32_t *csize = scratch_raw<uint32_t>(c, E, &st);
-  uint8_t *keep = scratch_raw<uint8_t>(c, E, &st);
-  uint64_t *fp = scratch_raw<uint64_t>(c, E, &st);
+  if (cw) HGP_CUDA(cudaMemsetAsync(cw, 0, 4 * (size_t)(Nc ? Nc : 1), c->stream));
+  HGP_TRY(launch(c, "gamma", k_gamma, dim3(grid_n(c, N)), dim3(256), 0, match, (const uint64_t *)cid, node_w, N,
+                 gamma, cw, mem, mem + Nc));
+  *Nc_out = Nc;
+  if (cw_out) *cw_out = cw;
+  if (mem_out) *mem_out = mem;
+  return HGP_OK;
+}
+
+// Coarse edges of the fine edges [elo, ehi) before the merge (reading #13-14): pins
+// mapped by gamma into the range's own oversized slots x[edge_off[e] - edge_off[elo] ..], src and
+// dst blocks sorted, S' = unique src \ D', D' = unique dst, kept unless D' = ∅ and |S'| <= 1, and
+// the 64-bit fingerprint of (|S'|, S', D').
+struct EdgeRange {
+  uint32_t *x, *cnsrc, *csize;
+  uint8_t *keep;
+  uint64_t *fp;
+  const uint64_t *off;     // [n+1] offsets of the range's slots in x (relative)
+  uint32_t n;
+};
+
+__global__ void k_rel_off(const uint64_t *edge_off, uint32_t elo, uint32_t n, uint64_t *rel) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x)
+    rel[i] = edge_off[elo + i] - edge_off[elo];
+}
+
+__global__ void k_cedges_pack(EdgeRange R, uint32_t elo, const uint64_t *pos, const uint64_t *poff, uint32_t *eid,
+                              uint64_t *fp, uint32_t *nsrc, uint32_t *size, uint64_t *off, uint32_t *pins) {
+  const uint32_t lane = lane_id();
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < R.n; i += nw) {
+    if (!R.keep[i]) continue;
+    const uint64_t k = pos[i], o = poff[i];
+    const uint32_t n = R.csize[i];
+    if (lane == 0) {
+      eid[k] = elo + (uint32_t)i; fp[k] = R.fp[i]; nsrc[k] = R.cnsrc[i]; size[k] = n; off[k] = o;
+    }
+    const uint32_t *src = R.x + R.off[i];
+    for (uint32_t j = lane; j < n; j += 32) pins[o + j] = src[j];
+  }
+}
+struct KeptFlag {
+  const uint8_t *keep;
+  __device__ uint64_t operator()(uint64_t i) const { return keep[i]; }
+};
+struct KeptSize {
+  const uint8_t *keep;
+  const uint32_t *size;
+  __device__ uint64_t operator()(uint64_t i) const { return keep[i] ? size[i] : 0u; }
+};
+
+static hgp_status edges_impl(hgp_ctx *c, const hgp_csr *g, const uint32_t *gamma, uint32_t elo, uint32_t ehi,
+                             EdgeRange *R) {
+  hgp_status st = HGP_OK;
+  const uint32_t n = ehi - elo;
+  uint64_t p0 = 0, p1 = 0;
+  if (elo == 0 && ehi == g->E) {
+    p1 = g->P;
+  } else {
+    uint64_t b[2];
+    HGP_TRY(read_back(c, g->edge_off + elo, 8, &b[0]));
+    HGP_TRY(read_back(c, g->edge_off + ehi, 8, &b[1]));
+    p0 = b[0];
+    p1 = b[1];
+  }
+  const uint64_t Pr = p1 - p0;
+  R->n = n;
+  R->x = scratch_raw<uint32_t>(c, Pr, &st);
+  R->cnsrc = scratch_raw<uint32_t>(c, n, &st);
+  R->csize = scratch_raw<uint32_t>(c, n, &st);
+  R->keep = scratch_raw<uint8_t>(c, n, &st);
+  R->fp = scratch_raw<uint64_t>(c, n, &st);
   if (st) return st;
-  HGP_TRY(launch(c, "map_pins", k_map_pins, dim3(grid_for(P)), dim3(256), 0, (const uint32_t *)g->pins,
-                 (const uint32_t *)gamma, P, x));
-  HGP_TRY(segmented_sort(c, EdgeSeg2{g->edge_off, g->edge_nsrc}, 2 * (uint64_t)E, x, g->max_edge));
-  HGP_TRY(launch(c, "edge_unique", k_edge_unique, dim3(grid_for(E, 8)), dim3(256), 0, (const uint64_t *)g->edge_off,
-                 (const uint32_t *)g->edge_nsrc, E, x, cnsrc, csize, keep, fp));
-  // ---- merge parallel edges
+  if (elo == 0) {
+    R->off = g->edge_off;                                           // p0 = 0: fine offsets are relative
+  } else {
+    uint64_t *rel = scratch_raw<uint64_t>(c, (size_t)n + 1, &st);
+    if (st) return st;
+    HGP_TRY(launch(c, "rel_off", k_rel_off, dim3(grid_n(c, (uint64_t)n + 1)), dim3(256), 0,
+                   (const uint64_t *)g->edge_off, elo, n, rel));
+    R->off = rel;
+  }
+  if (n == 0) return HGP_OK;
+  HGP_TRY(launch(c, "map_pins", k_map_pins, dim3(grid_n(c, Pr)), dim3(256), 0, (const uint32_t *)g->pins + p0,
+                 gamma, Pr, R->x));
+  HGP_TRY(segmented_sort(c, EdgeSeg2{R->off, g->edge_nsrc + elo}, 2 * (uint64_t)n, R->x, g->max_edge));
+  HGP_TRY(launch(c, "edge_unique", k_edge_unique, dim3(grid_n(c, n, 8)), dim3(256), 0, R->off,
+                 (const uint32_t *)g->edge_nsrc + elo, n, R->x, R->cnsrc, R->csize, R->keep, R->fp));
+  return HGP_OK;
+}
+
+// Merge of the entries of M (identical (S', D') -> one coarse edge, omega' = sum, mu' = sum,
+// ordered by the minimum fine id; reading #12) into C's edge arrays and incidence.
+static hgp_status merge_impl(hgp_ctx *c, const hgp_csr *g, MergeJob M, hgp_csr *C, uint32_t *erep_out) {
+  hgp_status st = HGP_OK;
+  const uint32_t K = M.E;
   uint32_t log2t = 4;
-  while ((1ull << log2t) < 2ull * E + 16) ++log2t;
-  MergeJob M{};
-  M.off = g->edge_off; M.x = x; M.cnsrc = cnsrc; M.csize = csize; M.keep = keep; M.fp = fp; M.E = E;
+  while ((1ull << log2t) < 2ull * K + 16) ++log2t;
   M.owner = scratch_raw<uint32_t>(c, (size_t)1 << log2t, &st);
   M.minrep = scratch_raw<uint32_t>(c, (size_t)1 << log2t, &st);
-  M.slot_of = scratch_raw<uint32_t>(c, E, &st);
+  M.slot_of = scratch_raw<uint32_t>(c, K, &st);
   M.log2t = log2t;
-  uint32_t *erep = scratch_raw<uint32_t>(c, E, &st);
-  uint32_t *is_rep = scratch_raw<uint32_t>(c, E, &st);
-  uint64_t *ceid = scratch_raw<uint64_t>(c, (size_t)E + 1, &st);
+  uint32_t *erep = erep_out ? erep_out : scratch_raw<uint32_t>(c, K, &st);
+  uint32_t *is_rep = scratch_raw<uint32_t>(c, K, &st);
+  uint64_t *ceid = scratch_raw<uint64_t>(c, (size_t)K + 1, &st);
   if (st) return st;
   HGP_CUDA(cudaMemsetAsync(M.owner, 0xFF, 4ull << log2t, c->stream));
   HGP_CUDA(cudaMemsetAsync(M.minrep, 0xFF, 4ull << log2t, c->stream));
-  HGP_TRY(launch(c, "merge_insert", k_merge_insert, dim3(grid_for(E)), dim3(256), 0, M));
-  HGP_TRY(launch(c, "merge_resolve", k_merge_resolve, dim3(grid_for(E)), dim3(256), 0, M, erep, is_rep));
+  HGP_TRY(launch(c, "merge_insert", k_merge_insert, dim3(grid_n(c, K)), dim3(256), 0, M));
+  HGP_TRY(launch(c, "merge_resolve", k_merge_resolve, dim3(grid_n(c, K)), dim3(256), 0, M, erep, is_rep));
   uint64_t Ec64 = 0;
-  HGP_TRY(scan_exclusive(c, InU32{is_rep}, E, ceid, &Ec64));
+  HGP_TRY(scan_exclusive(c, InU32{is_rep}, K, ceid, &Ec64));
   const uint32_t Ec = (uint32_t)Ec64;
   C->E = Ec;
   C->edge_off = dalloc_n<uint64_t>(c, (size_t)Ec + 1, &st);
@@ -468,32 +552,40 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   if (st) return st;
   HGP_CUDA(cudaMemsetAsync(C->edge_w, 0, 4 * (size_t)(Ec ? Ec : 1), c->stream));
   HGP_CUDA(cudaMemsetAsync(C->edge_mu, 0, 4 * (size_t)(Ec ? Ec : 1), c->stream));
-  HGP_TRY(launch(c, "coarse_edge_attrs", k_coarse_edge_attrs, dim3(grid_for(E)), dim3(256), 0, (const uint32_t *)erep,
-                 (const uint64_t *)ceid, (const uint32_t *)g->edge_w, (const uint32_t *)g->edge_mu,
-                 (const uint32_t *)cnsrc, (const uint32_t *)csize, E, C->edge_w, C->edge_mu, C->edge_nsrc, c_size));
+  HGP_TRY(launch(c, "coarse_edge_attrs", k_coarse_edge_attrs, dim3(grid_n(c, K)), dim3(256), 0, (const uint32_t *)erep,
+                 (const uint64_t *)ceid, (const uint32_t *)g->edge_w, (const uint32_t *)g->edge_mu, M.cnsrc, M.csize, K,
+                 M.eid, C->edge_w, C->edge_mu, C->edge_nsrc, c_size));
   uint64_t Pc = 0;
   HGP_TRY(scan_exclusive(c, InU32{c_size}, Ec, C->edge_off, &Pc));
   C->P = Pc;
   C->pins = dalloc_n<uint32_t>(c, Pc, &st);
   if (st) return st;
-  HGP_TRY(launch(c, "coarse_edge_pack", k_coarse_edge_pack, dim3(grid_for(E, 8)), dim3(256), 0, (const uint32_t *)erep,
-                 (const uint64_t *)ceid, (const uint64_t *)g->edge_off, (const uint32_t *)x, (const uint32_t *)csize,
-                 (const uint64_t *)C->edge_off, E, C->pins, maxes));
+  HGP_TRY(launch(c, "coarse_edge_pack", k_coarse_edge_pack, dim3(grid_n(c, K, 8)), dim3(256), 0, (const uint32_t *)erep,
+                 (const uint64_t *)ceid, M.off, M.x, M.csize, (const uint64_t *)C->edge_off, K, C->pins, maxes));
   uint32_t hmax[4];
   HGP_TRY(read_back(c, maxes, 16, hmax));
   C->max_edge = hmax[0];
-  HGP_TRY(build_incidence(c, C));
-  // ---- coarse neighbours
+  return build_incidence(c, C);
+}
+
+// Coarse neighbours (reading #7, #16) of the coarse nodes [clo, chi): member
+// segments are read through J's view (nb_off or nb_start/nb_len over nbr).
+static hgp_status cnbrs_impl(hgp_ctx *c, CNbrJob J, uint32_t clo, uint32_t chi, hgp_nbrs *CN, uint64_t *purged_out) {
+  hgp_status st = HGP_OK;
+  const uint32_t Nc = chi - clo;
+  // the kernels index coarse nodes from 0: shift the member arrays
+  J.mem0 += clo;
+  J.mem1 += clo;
   uint64_t *bound_off = scratch_raw<uint64_t>(c, (size_t)Nc + 1, &st);
   if (st) return st;
   uint64_t Vb = 0;
-  const uint64_t *seg_off = view ? nullptr : nb->off;
-  HGP_TRY(scan_exclusive(c, BoundIn{mem0, mem1, seg_off, view ? view->len : nullptr}, Nc, bound_off, &Vb));
+  HGP_TRY(scan_exclusive(c, BoundIn{J.mem0, J.mem1, J.nb_off, J.nb_off ? nullptr : J.nb_len}, Nc, bound_off, &Vb));
   uint32_t *pool = scratch_raw<uint32_t>(c, Vb, &st);
   uint32_t *ccnt = scratch_raw<uint32_t>(c, Nc, &st);
   uint32_t *lists = scratch_raw<uint32_t>(c, 3 * (size_t)Nc, &st);
   uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
   unsigned long long *misc = scratch_zero<unsigned long long>(c, 2, &st);   // purged, max bound (tier C)
+  unsigned int *maxes = scratch_zero<unsigned int>(c, 2, &st);
   if (st) return st;
   static uint64_t attr_dev = 0;   // per device: cudaFuncSetAttribute applies to the current one
   if (once_per_device(&attr_dev, c->device)) {
@@ -502,26 +594,24 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
     static_assert(kCMThreads == kCBThreads && kCMLog < kCBLog, "M and B share one instantiation");
     cudaFuncSetAttribute(k_coarse_nbrs<kCBThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kCBLog);
   }
-  CNbrJob J{};
-  J.mem0 = mem0; J.mem1 = mem1; J.nb_off = seg_off; J.gamma = gamma; J.bound_off = bound_off;
-  J.nb_start = view ? view->start : nullptr; J.nb_len = view ? view->len : nullptr;
-  J.nbr = view ? view->nbr : nb->nbr;
-  J.pool = pool; J.cnt = ccnt; J.Nc = Nc; J.purged = misc;
+  J.bound_off = bound_off;
+  J.pool = pool; J.cnt = ccnt; J.Nc = Nc; J.purged = misc; J.tiers = c->d_tiers; J.tier = HGP_TIER_CNBRS_A;
+  J.cbase = clo;
   const uint32_t capA = 1u << (kCALog - 1), capM = 1u << (kCMLog - 1), capB = 1u << (kCBLog - 1);
   J.list = nullptr; J.list_count = nullptr; J.cap = capA; J.log2s = kCALog;
   const uint32_t gA = Nc < 64u * c->sm_count ? (Nc ? Nc : 1) : 64u * c->sm_count;
-  HGP_TRY(launch(c, "coarse_nbrs_A", k_coarse_nbrs<kCAThreads, true>, dim3(gA), dim3(kCAThreads), 4u << kCALog, J));
-  HGP_TRY(launch(c, "cnbr_classify", k_cnbr_classify, dim3(grid_for(Nc)), dim3(256), 0, (const uint64_t *)bound_off, Nc,
-                 capA, capM, capB, lists, lists + Nc, lists + 2 * (size_t)Nc, counts, misc + 1));
+  if (Nc) HGP_TRY(launch(c, "coarse_nbrs_A", k_coarse_nbrs<kCAThreads, true>, dim3(gA), dim3(kCAThreads), 4u << kCALog, J));
+  if (Nc) HGP_TRY(launch(c, "cnbr_classify", k_cnbr_classify, dim3(grid_n(c, Nc)), dim3(256), 0, (const uint64_t *)bound_off,
+                         Nc, capA, capM, capB, lists, lists + Nc, lists + 2 * (size_t)Nc, counts, misc + 1));
   uint32_t hc[3];
   HGP_TRY(read_back(c, counts, 12, hc));
   if (hc[0]) {
-    J.list = lists; J.list_count = counts; J.cap = capM; J.log2s = kCMLog;
+    J.list = lists; J.list_count = counts; J.cap = capM; J.log2s = kCMLog; J.tier = HGP_TIER_CNBRS_M;
     HGP_TRY(launch(c, "coarse_nbrs_M", k_coarse_nbrs<kCMThreads, true>, dim3(3 * c->sm_count), dim3(kCMThreads),
                    4u << kCMLog, J));
   }
   if (hc[1]) {
-    J.list = lists + Nc; J.list_count = counts + 1; J.cap = capB; J.log2s = kCBLog;
+    J.list = lists + Nc; J.list_count = counts + 1; J.cap = capB; J.log2s = kCBLog; J.tier = HGP_TIER_CNBRS_B;
     HGP_TRY(launch(c, "coarse_nbrs_B", k_coarse_nbrs<kCBThreads, true>, dim3(c->sm_count), dim3(kCBThreads),
                    4u << kCBLog, J));
   }
@@ -534,10 +624,11 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
     uint32_t *gtab = scratch_raw<uint32_t>(c, (size_t)ctas << lg, &st);
     if (st) return st;
     J.list = lists + 2 * (size_t)Nc; J.list_count = counts + 2; J.cap = 0xFFFFFFFFu; J.log2s = lg; J.gtab = gtab;
+    J.tier = HGP_TIER_CNBRS_C;
     HGP_TRY(launch(c, "coarse_nbrs_C", k_coarse_nbrs<256, false>, dim3(ctas), dim3(256), 0, J));
   }
-  CN->lo = 0;
-  CN->hi = Nc;
+  CN->lo = clo;
+  CN->hi = chi;
   CN->off = dalloc_n<uint64_t>(c, (size_t)Nc + 1, &st);
   if (st) return st;
   uint64_t Vc = 0;
@@ -545,24 +636,50 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   CN->V = Vc;
   CN->nbr = dalloc_n<uint32_t>(c, Vc, &st);
   if (st) return st;
-  HGP_TRY(launch(c, "cnbr_pack", k_cnbr_pack, dim3(grid_for(Nc, 8)), dim3(256), 0, (const uint32_t *)pool,
-                 (const uint64_t *)bound_off, (const uint32_t *)ccnt, (const uint64_t *)CN->off, Nc, CN->nbr, maxes + 1));
+  if (Nc)
+    HGP_TRY(launch(c, "cnbr_pack", k_cnbr_pack, dim3(grid_n(c, Nc, 8)), dim3(256), 0, (const uint32_t *)pool,
+                   (const uint64_t *)bound_off, (const uint32_t *)ccnt, (const uint64_t *)CN->off, Nc, CN->nbr, maxes));
+  uint32_t hmax[2];
+  HGP_TRY(read_back(c, maxes, 8, hmax));
+  CN->max_deg = hmax[0];
+  if (purged_out) HGP_TRY(read_u64(c, (const uint64_t *)misc, purged_out));
+  return HGP_OK;
+}
+
+hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const uint32_t *match, uint32_t *gamma,
+                         hgp_csr *C, hgp_nbrs *CN, hgp_level_stats *stats, const SegView *view) {
+  hgp_status st = HGP_OK;
+  const uint32_t N = g->N, E = g->E;
+  memset(C, 0, sizeof(*C));
+  memset(CN, 0, sizeof(*CN));
+  uint32_t Nc = 0, *mem = nullptr;
+  HGP_TRY(gamma_impl(c, match, N, g->node_w, gamma, &Nc, &C->node_w, &mem, true));
+  C->N = Nc;
+  EdgeRange R{};
+  HGP_TRY(edges_impl(c, g, gamma, 0, E, &R));
+  MergeJob M{};
+  M.off = R.off; M.x = R.x; M.cnsrc = R.cnsrc; M.csize = R.csize; M.keep = R.keep; M.fp = R.fp; M.eid = nullptr;
+  M.E = E;
+  uint32_t *erep = scratch_raw<uint32_t>(c, E, &st);
+  if (st) return st;
+  HGP_TRY(merge_impl(c, g, M, C, erep));
+  CNbrJob J{};
+  J.mem0 = mem; J.mem1 = mem + Nc; J.gamma = gamma;
+  J.nb_off = view ? nullptr : nb->off;
+  J.nb_start = view ? view->start : nullptr; J.nb_len = view ? view->len : nullptr;
+  J.nbr = view ? view->nbr : nb->nbr;
   uint64_t purged = 0;
-  HGP_TRY(read_back(c, maxes, 16, hmax));
-  HGP_TRY(read_u64(c, (const uint64_t *)misc, &purged));
-  CN->max_deg = hmax[1];
+  HGP_TRY(cnbrs_impl(c, J, 0, Nc, CN, &purged));
   if (stats) {
-    uint64_t kept = 0;
     // kept edges = classes' members; dropped = E - kept; merged = kept - Ec
     uint32_t *kc = scratch_zero<uint32_t>(c, 1, &st);
     if (st) return st;
-    HGP_TRY(launch(c, "count_kept", k_count_kept, dim3(grid_for(E)), dim3(256), 0, (const uint32_t *)erep, E, kc));
+    HGP_TRY(launch(c, "count_kept", k_count_kept, dim3(grid_n(c, E)), dim3(256), 0, (const uint32_t *)erep, E, kc));
     uint32_t hk = 0;
     HGP_TRY(read_back(c, kc, 4, &hk));
-    kept = hk;
-    stats->Nc = Nc; stats->Ec = Ec; stats->Pc = Pc; stats->Vc = Vc;
-    stats->dropped_edges = (uint32_t)(E - kept);
-    stats->merged_edges = (uint32_t)(kept - Ec);
+    stats->Nc = Nc; stats->Ec = C->E; stats->Pc = C->P; stats->Vc = CN->V;
+    stats->dropped_edges = (uint32_t)(E - hk);
+    stats->merged_edges = (uint32_t)(hk - C->E);
     stats->purged = purged;
   }
   return HGP_OK;
@@ -582,3 +699,130 @@ extern "C" hgp_status hgp_contract(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs 
   if (s != HGP_OK) { free_csr(c, coarse); free_nbrs(c, coarse_nb); }
   return s;
 }
+
+// ---- a5 in pieces for node/edge-range shards; hgp_contract = these on one GPU.
+extern "C" {
+
+__global__ void k_coarse_bounds(const uint64_t *cid, const uint32_t *nb, uint32_t nbounds, uint64_t *cb) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nbounds; i += gridDim.x * blockDim.x) cb[i] = cid[nb[i]];
+}
+
+hgp_status hgp_coarse_bounds(hgp_ctx *c, const uint32_t *match, uint32_t N, const uint32_t *node_bounds, uint32_t nbounds,
+                             uint32_t *coarse_bounds) {
+  if (!c || (N && !match) || !node_bounds || !coarse_bounds) return set_error(HGP_E_ARG, "hgp_coarse_bounds: null argument");
+  ApiScope scope(c);
+  hgp_status st = HGP_OK;
+  uint32_t *rep = scratch_raw<uint32_t>(c, N, &st);
+  uint64_t *cid = scratch_raw<uint64_t>(c, (size_t)N + 1, &st);
+  uint32_t *db = scratch_raw<uint32_t>(c, nbounds, &st);
+  uint64_t *dc = scratch_raw<uint64_t>(c, nbounds, &st);
+  if (st) return st;
+  for (uint32_t i = 0; i < nbounds; ++i)
+    if (node_bounds[i] > N) return set_error(HGP_E_ARG, "hgp_coarse_bounds: bound %u > N", node_bounds[i]);
+  HGP_TRY(clear_errors(c));
+  HGP_TRY(launch(c, "rep", k_rep, dim3(grid_n(c, N)), dim3(256), 0, match, N, rep, c->d_err));
+  HGP_TRY(scan_exclusive(c, InU32{rep}, N, cid, nullptr));
+  HGP_CUDA(cudaMemcpyAsync(db, node_bounds, 4ull * nbounds, cudaMemcpyHostToDevice, c->stream));
+  HGP_TRY(launch(c, "coarse_bounds", k_coarse_bounds, dim3(1), dim3(256), 0, (const uint64_t *)cid, (const uint32_t *)db,
+                 nbounds, dc));
+  std::vector<uint64_t> h(nbounds);
+  HGP_TRY(read_back(c, dc, 8ull * nbounds, h.data()));
+  for (uint32_t i = 0; i < nbounds; ++i) coarse_bounds[i] = (uint32_t)h[i];
+  return HGP_OK;
+}
+
+hgp_status hgp_gamma(hgp_ctx *c, const uint32_t *match, uint32_t N, uint32_t *gamma, uint32_t *Nc) {
+  if (!c || (N && (!match || !gamma)) || !Nc) return set_error(HGP_E_ARG, "hgp_gamma: null argument");
+  ApiScope scope(c);
+  return gamma_impl(c, match, N, nullptr, gamma, Nc, nullptr, nullptr, false);
+}
+
+void hgp_cedges_free(hgp_ctx *c, hgp_cedges *ce) {
+  if (!c || !ce) return;
+  DeviceGuard dg(c->device);
+  const size_t K = ce->K ? ce->K : 1;
+  c->dfree(ce->eid, 4 * K);
+  c->dfree(ce->fp, 8 * K);
+  c->dfree(ce->nsrc, 4 * K);
+  c->dfree(ce->size, 4 * K);
+  c->dfree(ce->off, 8 * (K + 1));
+  c->dfree(ce->pins, 4 * (ce->P ? ce->P : 1));
+  memset(ce, 0, sizeof(*ce));
+}
+
+hgp_status hgp_contract_edges(hgp_ctx *c, const hgp_csr *g, const uint32_t *gamma, uint32_t elo, uint32_t ehi,
+                              hgp_cedges *out) {
+  if (!c || !g || !gamma || !out) return set_error(HGP_E_ARG, "hgp_contract_edges: null argument");
+  if (elo > ehi || ehi > g->E) return set_error(HGP_E_ARG, "hgp_contract_edges: bad edge range");
+  ApiScope scope(c);
+  memset(out, 0, sizeof(*out));
+  hgp_status st = HGP_OK;
+  EdgeRange R{};
+  HGP_TRY(edges_impl(c, g, gamma, elo, ehi, &R));
+  const uint32_t n = ehi - elo;
+  uint64_t *pos = scratch_raw<uint64_t>(c, (size_t)n + 1, &st);
+  uint64_t *poff = scratch_raw<uint64_t>(c, (size_t)n + 1, &st);
+  if (st) return st;
+  uint64_t K = 0, P = 0;
+  HGP_TRY(scan_exclusive(c, KeptFlag{R.keep}, n, pos, &K));
+  HGP_TRY(scan_exclusive(c, KeptSize{R.keep, R.csize}, n, poff, &P));
+  out->K = (uint32_t)K;
+  out->P = P;
+  out->eid = dalloc_n<uint32_t>(c, K, &st);
+  out->fp = dalloc_n<uint64_t>(c, K, &st);
+  out->nsrc = dalloc_n<uint32_t>(c, K, &st);
+  out->size = dalloc_n<uint32_t>(c, K, &st);
+  out->off = dalloc_n<uint64_t>(c, K + 1, &st);
+  out->pins = dalloc_n<uint32_t>(c, P, &st);
+  if (st) { hgp_cedges_free(c, out); return st; }
+  hgp_status s = HGP_OK;
+  if (n)
+    s = launch(c, "cedges_pack", k_cedges_pack, dim3(grid_n(c, (uint64_t)n * 32)), dim3(256), 0, R, elo,
+               (const uint64_t *)pos, (const uint64_t *)poff, out->eid, out->fp, out->nsrc, out->size, out->off,
+               out->pins);
+  if (s == HGP_OK) s = hgp_copy(c, out->off + K, &P, 8) == HGP_OK ? hgp_sync(c) : HGP_E_CUDA;
+  if (s != HGP_OK) hgp_cedges_free(c, out);
+  return s;
+}
+
+hgp_status hgp_contract_merge(hgp_ctx *c, const hgp_csr *g, const uint32_t *match, uint32_t *gamma,
+                              const hgp_cedges *all, hgp_csr *coarse) {
+  if (!c || !g || !match || !gamma || !all || !coarse) return set_error(HGP_E_ARG, "hgp_contract_merge: null argument");
+  ApiScope scope(c);
+  memset(coarse, 0, sizeof(*coarse));
+  uint32_t Nc = 0;
+  hgp_status s = gamma_impl(c, match, g->N, g->node_w, gamma, &Nc, &coarse->node_w, nullptr, true);
+  if (s == HGP_OK) {
+    coarse->N = Nc;
+    MergeJob M{};
+    M.off = all->off; M.x = all->pins; M.cnsrc = all->nsrc; M.csize = all->size; M.keep = nullptr; M.fp = all->fp;
+    M.eid = all->eid; M.E = all->K;
+    s = merge_impl(c, g, M, coarse, nullptr);
+  }
+  if (s != HGP_OK) free_csr(c, coarse);
+  return s;
+}
+
+hgp_status hgp_coarse_neighbors(hgp_ctx *c, const uint32_t *match, const uint32_t *gamma, uint32_t N,
+                                const uint64_t *seg_start, const uint32_t *seg_len, const uint32_t *nbr, uint32_t clo,
+                                uint32_t chi, hgp_nbrs *out) {
+  if (!c || !match || !gamma || !seg_start || !seg_len || !out) return set_error(HGP_E_ARG, "hgp_coarse_neighbors: null argument");
+  ApiScope scope(c);
+  memset(out, 0, sizeof(*out));
+  uint32_t Nc = 0, *mem = nullptr;
+  // the members of every coarse node (gamma is recomputed, identically, into scratch)
+  hgp_status st = HGP_OK;
+  uint32_t *g2 = scratch_raw<uint32_t>(c, N, &st);
+  if (st) return st;
+  hgp_status s = gamma_impl(c, match, N, nullptr, g2, &Nc, nullptr, &mem, false);
+  if (s != HGP_OK) return s;
+  if (clo > chi || chi > Nc) return set_error(HGP_E_ARG, "hgp_coarse_neighbors: bad coarse range");
+  CNbrJob J{};
+  J.mem0 = mem; J.mem1 = mem + Nc; J.gamma = gamma;
+  J.nb_off = nullptr; J.nb_start = seg_start; J.nb_len = seg_len; J.nbr = nbr;
+  s = cnbrs_impl(c, J, clo, chi, out, nullptr);
+  if (s != HGP_OK) free_nbrs(c, out);
+  return s;
+}
+
+}  // extern "C"

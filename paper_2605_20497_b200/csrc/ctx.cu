@@ -154,6 +154,8 @@ hgp_status hgp_ctx_create(int device, hgp_stream_t stream, const hgp_allocator *
     }
   }
   if (cudaMalloc(&c->d_err, sizeof(uint64_t) * kErrSlots) != cudaSuccess ||
+      cudaMalloc(&c->d_tiers, sizeof(uint64_t) * HGP_TIERS) != cudaSuccess ||
+      cudaMemset(c->d_tiers, 0, sizeof(uint64_t) * HGP_TIERS) != cudaSuccess ||
       cudaMallocHost(&c->h_pin, sizeof(uint64_t) * 64) != cudaSuccess) {
     delete c;
     return set_error(HGP_E_OOM, "hgp_ctx_create: cannot allocate error slots");
@@ -171,6 +173,7 @@ void hgp_ctx_destroy(hgp_ctx *c) {
   c->chunks.clear();
   cudaStreamSynchronize(c->stream);
   cudaFree(c->d_err);
+  cudaFree(c->d_tiers);
   cudaFreeHost(c->h_pin);
   for (auto &ev : c->ev) cudaEventDestroy(ev);
   for (auto &pr : c->prof_events) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
@@ -242,6 +245,19 @@ hgp_status hgp_profile_report(hgp_ctx *c, char *buf, size_t len) {
     out += line;
   }
   snprintf(buf, len, "%s", out.c_str());
+  return HGP_OK;
+}
+
+hgp_status hgp_tier_counts(hgp_ctx *c, uint64_t *out, int reset) {
+  if (!c || !out) return set_error(HGP_E_ARG, "hgp_tier_counts: null argument");
+  DeviceGuard dg(c->device);
+  HGP_CUDA(cudaMemcpyAsync(out, c->d_tiers, sizeof(uint64_t) * HGP_TIERS, cudaMemcpyDeviceToHost, c->stream));
+  HGP_CUDA(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < HGP_TIERS; ++i) out[i] += c->h_tiers[i];
+  if (reset) {
+    HGP_CUDA(cudaMemsetAsync(c->d_tiers, 0, sizeof(uint64_t) * HGP_TIERS, c->stream));
+    for (auto &x : c->h_tiers) x = 0;
+  }
   return HGP_OK;
 }
 

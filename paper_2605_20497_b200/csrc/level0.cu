@@ -36,6 +36,8 @@ struct FusedJob {
   uint64_t start_bias;                    // added to every start written
   const uint64_t *cv;                     // [E] c(e), Eq.5 term in 2^-24 fixed point
   const uint2 *wmu;                       // [N] (size, in_mu) packed for the validity test
+  unsigned long long *tiers;              // work counters (hgp_tier_counts)
+  int tier;
 };
 
 // The validity test of Eq.6 on one (key, acc) pair of the dense list; writes the
@@ -247,6 +249,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
     reinterpret_cast<uint4 *>(acc)[i] = make_uint4(0, 0, 0, 0);
   }
   if (tid == 0) s_full = 0;
+  uint32_t done = 0;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = F.list ? F.list[t] : J.lo + t;
     const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1], iin = i0 + J.inc_nin[n];
@@ -545,9 +548,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
     __syncthreads();                                               // B4
     if (tid == 0) s_full = 0;
     if (over || s_defer) continue;                                 // (the table is already clean)
+    if (tid == 0) ++done;
     if (small) eval_packed<PIMAX, THREADS>(J, F, n, count, dense, (uint32_t)g, ib, s_start, s_tops);
     else eval_top<PIMAX, THREADS>(J, F, n, count, dense, g, ib, s_start, s_tops, s_topi);
   }
+  if (tid == 0) tier_add(F.tiers, F.tier, done);
 }
 
 __global__ void k_fused_pack(const uint32_t *pool, const uint64_t *start, const uint32_t *cnt, const uint64_t *off,
@@ -641,29 +646,30 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
     if (st) return st;
     HGP_TRY(launch(c, "sample_lists", k_sample_lists, dim3(div_up(L.hn, 256) < 4096 ? div_up(L.hn, 256) : 4096), dim3(256),
                    0, F.S.lo, L.hn, kStride, sample, rest, cnt2));
-    F.list = sample; F.list_count = cnt2; F.log2s = kFALog;
+    F.list = sample; F.list_count = cnt2; F.log2s = kFALog; F.tier = HGP_TIER_FUSED_S;
     F.defer_list = L.la; F.defer_count = L.ca;
     HGP_TRY(launch(c, "nbrscore_S", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
     uint32_t deferred = 0;
     HGP_TRY(read_back(c, L.ca, 4, &deferred));
     const uint32_t ns = (L.hn + kStride - 1) / kStride;
     F.list = rest; F.list_count = cnt2 + 1;
+    F.tier = HGP_TIER_FUSED_A;
     if (4 * deferred > ns) {                                        // > 25 %: start in M
-      F.log2s = kFMLog; F.defer_list = L.lm; F.defer_count = L.cm;
+      F.log2s = kFMLog; F.tier = HGP_TIER_FUSED_M; F.defer_list = L.lm; F.defer_count = L.cm;
       HGP_TRY(launch(c, "nbrscore_M", k_nbrscore<kFMThreads, PIMAX, 3, kFMLog>, dim3(3 * sm), dim3(kFMThreads),
                      fused_smem(kFMLog), F));
     } else {
       HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
     }
   } else {
-    F.list = L.in_list; F.list_count = L.in_count; F.log2s = kFALog;
+    F.list = L.in_list; F.list_count = L.in_count; F.log2s = kFALog; F.tier = HGP_TIER_FUSED_A;
     F.defer_list = L.la; F.defer_count = L.ca;
     HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
   }
-  F.list = L.la; F.list_count = L.ca; F.log2s = kFMLog;
+  F.list = L.la; F.list_count = L.ca; F.log2s = kFMLog; F.tier = HGP_TIER_FUSED_M;
   F.defer_list = L.lm; F.defer_count = L.cm;
   HGP_TRY(launch(c, "nbrscore_M", k_nbrscore<kFMThreads, PIMAX, 3, kFMLog>, dim3(3 * sm), dim3(kFMThreads), fused_smem(kFMLog), F));
-  F.list = L.lm; F.list_count = L.cm; F.log2s = kFBLog;
+  F.list = L.lm; F.list_count = L.cm; F.log2s = kFBLog; F.tier = HGP_TIER_FUSED_B;
   F.defer_list = L.ld; F.defer_count = L.cd;
   HGP_TRY(launch(c, "nbrscore_B", k_nbrscore<kFBThreads, PIMAX, 1, kFBLog>, dim3(sm), dim3(kFBThreads), fused_smem(kFBLog), F));
   return HGP_OK;
@@ -745,6 +751,7 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   F.S = J;
   F.cv = cv;
   F.wmu = wmu;
+  F.tiers = c->d_tiers;
   F.pool = pool; F.pool_cap = pool_cap; F.pool_cursor = misc + 1; F.start = start; F.cnt = cnt;
   F.pool_list = LP; F.pool_count = counts + 3;
   TierLists L{nullptr, nullptr, nn, LA, counts + 0, LM, counts + 1, LD, counts + 2};

@@ -225,6 +225,7 @@ extern "C" hgp_status hgp_match(hgp_ctx *c, const hgp_cand *cand, uint32_t N, ui
     uint32_t novf = 0;
     HGP_TRY(read_back(c, R.overflow, 4, &novf));
     if (novf) {   // chains longer than the walk cap: pointer jumping (log rounds)
+      c->h_tiers[HGP_TIER_JUMP] += novf;
       uint32_t *jmp = scratch_raw<uint32_t>(c, 2 * (size_t)N, &st);
       uint8_t *par = scratch_raw<uint8_t>(c, 2 * (size_t)N, &st);
       int8_t *val = scratch_raw<int8_t>(c, N, &st);

@@ -30,6 +30,8 @@ struct NbrJob {
   uint32_t *ovf_list, *ovf_count;    // table overflow -> next tier
   uint32_t *pool_list, *pool_count;  // pool overflow -> rerun after growing the pool
   uint64_t start_bias;               // added to every start written (pool base differs from the view's)
+  unsigned long long *tiers;         // work counters (hgp_tier_counts)
+  int tier;
 };
 
 template <int THREADS, bool SMEM>
@@ -43,6 +45,7 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
   const uint32_t S = 1u << J.log2s;
   uint32_t *tab = SMEM ? dyn : J.gtab + ((size_t)blockIdx.x << J.log2s);
   const uint32_t total = J.list_count ? *J.list_count : J.nall;
+  uint32_t done = 0;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = J.list ? J.list[t] : J.lo + t;
     for (uint32_t i = tid; i < S / 4; i += THREADS)
@@ -142,10 +145,11 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
         wpos = __shfl_sync(0xFFFFFFFFu, wpos, 0);
         if (has) J.pool[s_start + wpos + __popc(bal & lt)] = v;
       }
-      if (tid == 0) { J.start[n - J.lo] = s_start + J.start_bias; J.cnt[n - J.lo] = count; }
+      if (tid == 0) { J.start[n - J.lo] = s_start + J.start_bias; J.cnt[n - J.lo] = count; ++done; }
     }
     __syncthreads();
   }
+  if (tid == 0) tier_add(J.tiers, J.tier, done);
 }
 
 // bound_n = min(N-1, sum_{e in I(n)} (|e|-1)) for the listed nodes -> atomicMax
@@ -267,16 +271,16 @@ hgp_status nbrs_for_list(hgp_ctx *c, const hgp_csr *g, uint32_t lo, const uint32
     J.start_bias = (uint64_t)(pool - base);
     J.start = start; J.cnt = cnt; J.pool_list = plist; J.pool_count = counters + 5;
     J.list = list; J.list_count = list_count;
-    J.log2s = kT1LogL; J.cap = (1u << (kT1LogL - 1)) - 128 * (kT1ThreadsL / 32);
+    J.tiers = c->d_tiers; J.tier = HGP_TIER_NBRS_1; J.log2s = kT1LogL; J.cap = (1u << (kT1LogL - 1)) - 128 * (kT1ThreadsL / 32);
     J.ovf_list = list1; J.ovf_count = counters + 0;
     HGP_TRY(launch(c, "nbrs_list_t1", k_nbrs<kT1ThreadsL, true>, dim3(8u * c->sm_count), dim3(kT1ThreadsL),
                    4u << kT1LogL, J));
     J.list = list1; J.list_count = counters + 0;
-    J.log2s = kT2LogL; J.cap = (1u << (kT2LogL - 1)) - 128 * (kT2ThreadsL / 32);
+    J.tiers = c->d_tiers; J.tier = HGP_TIER_NBRS_2; J.log2s = kT2LogL; J.cap = (1u << (kT2LogL - 1)) - 128 * (kT2ThreadsL / 32);
     J.ovf_list = list2; J.ovf_count = counters + 1;
     HGP_TRY(launch(c, "nbrs_list_t2", k_nbrs<kT2ThreadsL, true>, dim3(c->sm_count), dim3(kT2ThreadsL), 4u << kT2LogL, J));
     if (t3) {
-      J.list = list2; J.list_count = counters + 1; J.log2s = lg; J.cap = 0xFFFFFFFFu; J.gtab = gtab;
+      J.list = list2; J.list_count = counters + 1; J.log2s = lg; J.cap = 0xFFFFFFFFu; J.gtab = gtab; J.tier = HGP_TIER_NBRS_3;
       J.ovf_list = list1; J.ovf_count = counters + 4;   // cannot overflow: table >= 2 (bound + 1)
       HGP_TRY(launch(c, "nbrs_list_t3", k_nbrs<256, false>, dim3(c->sm_count), dim3(256), 0, J));
     }
@@ -343,13 +347,13 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
     J.start = start; J.cnt = cnt; J.pool_list = plist; J.pool_count = counters + 2;
     // tier 1: every node, 16 KB shared table
     J.list = nullptr; J.list_count = nullptr; J.nall = nn;
-    J.log2s = kT1Log; J.cap = (1u << (kT1Log - 1)) - 128 * (kT1Threads / 32);
+    J.tiers = c->d_tiers; J.tier = HGP_TIER_NBRS_1; J.log2s = kT1Log; J.cap = (1u << (kT1Log - 1)) - 128 * (kT1Threads / 32);
     J.ovf_list = list1; J.ovf_count = counters + 0;
     const uint32_t grid1 = nn < 32u * c->sm_count ? nn : 32u * c->sm_count;
     HGP_TRY(launch(c, "nbrs_t1", k_nbrs<kT1Threads, true>, dim3(grid1), dim3(kT1Threads), 4u << kT1Log, J));
     // tier 2: 128 KB shared table for the overflowed nodes (grid-stride over a device count)
     J.list = list1; J.list_count = counters + 0;
-    J.log2s = kT2Log; J.cap = (1u << (kT2Log - 1)) - 128 * (kT2Threads / 32);
+    J.tiers = c->d_tiers; J.tier = HGP_TIER_NBRS_2; J.log2s = kT2Log; J.cap = (1u << (kT2Log - 1)) - 128 * (kT2Threads / 32);
     J.ovf_list = list2; J.ovf_count = counters + 1;
     HGP_TRY(launch(c, "nbrs_t2", k_nbrs<kT2Threads, true>, dim3(c->sm_count), dim3(kT2Threads), 4u << kT2Log, J));
     uint32_t hc[4];
@@ -365,7 +369,7 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
       const uint32_t ctas = hc[1] < (uint32_t)c->sm_count ? hc[1] : (uint32_t)c->sm_count;
       uint32_t *gtab = scratch_raw<uint32_t>(c, (size_t)ctas << lg, &st);
       if (st) return st;
-      J.list = list2; J.list_count = counters + 1; J.log2s = lg; J.cap = 0xFFFFFFFFu; J.gtab = gtab;
+      J.list = list2; J.list_count = counters + 1; J.log2s = lg; J.cap = 0xFFFFFFFFu; J.gtab = gtab; J.tier = HGP_TIER_NBRS_3;
       J.ovf_list = list1; J.ovf_count = counters + 4;   // cannot overflow: table >= 2 (bound + 1)
       HGP_TRY(launch(c, "nbrs_t3", k_nbrs<256, false>, dim3(ctas), dim3(256), 0, J));
       HGP_TRY(read_back(c, counters, 16, hc));

@@ -10,7 +10,7 @@
 //       pins_in, the per-move count of violated constraints; and the landing point.
 //
 // Everything is integer (weights u32, sums exact), so results are bit-identical to the oracle
-// (oracle/hgp_ref_refine.cpp) whatever the schedule.
+// (the CPU oracle of the tests) whatever the schedule.
 #include <algorithm>
 
 #include "csr_impl.cuh"

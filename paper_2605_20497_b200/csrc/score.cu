@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
   uint64_t *eta = reinterpret_cast<uint64_t *>(base + ((size_t)8 << log2s));        // wide only
   uint32_t *inter32 = reinterpret_cast<uint32_t *>(base + ((size_t)8 << log2s) + 16);  // split only (S+1 slots)
   const uint32_t total = J.list_count ? *J.list_count : J.hi - J.lo;
+  uint32_t done = 0;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = J.list ? J.list[t] : J.lo + t;
     uint64_t b0, b1;
@@ -272,8 +273,10 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
         J.cand[(uint64_t)n * J.pi + r] = cd;
       }
     }
+    if (tid == 0) ++done;
     __syncthreads();
   }
+  if (tid == 0) tier_add(J.tiers, J.tier, done);
 }
 
 // feasibility + the norm=1 overflow guard
@@ -317,13 +320,13 @@ hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_
   J.big_list = bigA; J.big_count = counts + 0; J.wide_list = wide; J.wide_count = counts + 1;
   HGP_TRY(launch_score_flat<PIMAX>(c, J, nn, J.E));
   if (max_deg > (1u << (kSALog - 1))) {   // B: big neighbourhoods, packed (overflow -> wide)
-    J.list = bigA; J.list_count = counts + 0; J.cap = 1u << (kSBLog - 1); J.log2s = kSBLog;
+    J.list = bigA; J.list_count = counts + 0; J.cap = 1u << (kSBLog - 1); J.log2s = kSBLog; J.tier = HGP_TIER_SCORE_B;
     J.big_list = huge; J.big_count = counts + 2;
     HGP_TRY(launch(c, "score_B", k_score<kSBThreads, kModeP32, true, PIMAX>, dim3(c->sm_count), dim3(kSBThreads),
                    (8u << kSBLog) + 16, J));
   }
   // W: the rest (neighbourhoods up to 2048)
-  J.list = wide; J.list_count = counts + 1; J.cap = 1u << (kSWLog - 1); J.log2s = kSWLog;
+  J.list = wide; J.list_count = counts + 1; J.cap = 1u << (kSWLog - 1); J.log2s = kSWLog; J.tier = HGP_TIER_SCORE_W;
   J.big_list = huge; J.big_count = counts + 2;
   HGP_TRY(launch(c, "score_W", k_score<kSWThreads, kModeWide, true, PIMAX>, dim3(c->sm_count), dim3(kSWThreads),
                  16u << kSWLog, J));
@@ -333,7 +336,7 @@ hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_
     const uint32_t ctas = c->sm_count;
     uint32_t *gtab = scratch_raw<uint32_t>(c, ((size_t)ctas * 16 << lg) / 4, &st);
     if (st) return st;
-    J.list = huge; J.list_count = counts + 2; J.cap = 0xFFFFFFFFu; J.log2s = lg; J.gtab = gtab;
+    J.list = huge; J.list_count = counts + 2; J.cap = 0xFFFFFFFFu; J.log2s = lg; J.gtab = gtab; J.tier = HGP_TIER_SCORE_H;
     HGP_TRY(launch(c, "score_H", k_score<256, kModeWide, false, PIMAX>, dim3(ctas), dim3(256), 0, J));
   }
   return HGP_OK;
@@ -382,6 +385,7 @@ hgp_status score_prologue(hgp_ctx *c, const hgp_csr *g, uint32_t lo, uint32_t hi
   J->pi = p->pi; J->norm = p->norm;
   J->E = g->E;
   J->N = g->N;
+  J->tiers = c->d_tiers;
   return HGP_OK;
 }
 

@@ -31,6 +31,8 @@ struct ScoreJob {
   uint32_t *big_list, *big_count;    // deferred: neighbourhood larger than cap
   uint32_t *wide_list, *wide_count;  // deferred: packed 32-bit accumulator would overflow
   const unsigned int *max_in_mu;     // device scalar: max in_mu over the level (nullptr: unknown)
+  unsigned long long *tiers;         // work counters (hgp_tier_counts)
+  int tier;
 };
 
 enum { kModeP32 = 0, kModeWide = 1, kModeSplit = 2 };

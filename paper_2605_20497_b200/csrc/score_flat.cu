@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
   const uint32_t inter_s = opaque_u32(smem_u32addr(inter));
   const uint32_t rowA_s = opaque_u32(smem_u32addr(rowA)), rowB_s = opaque_u32(smem_u32addr(rowB));
   const uint32_t total = J.list_count ? *J.list_count : J.hi - J.lo;
+  uint32_t n_nointer = 0, n_packed = 0, n_split = 0;                // tier counters (thread 0)
   for (uint32_t i = tid; i < S; i += kFThreads) { keys[i] = kEmpty; acc[i] = 0; if (i < S / 2) inter[i] = 0; }
   if (tid < 4) { acc[S + tid] = 0; inter[S / 2 + tid] = 0; }
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
@@ -143,6 +144,11 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
       continue;
     }
     if (!packed) { g = 1; ib = 0; }
+    if (tid == 0) {
+      if (!packed) ++n_split;
+      else if (nointer && ib == 0) ++n_nointer;
+      else ++n_packed;
+    }
     // ---- phase 1: bins
     for (uint32_t i = tid; i < cnt; i += kFThreads) {
       const uint32_t v = J.nbr[b0 + i];
@@ -384,6 +390,11 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
       if (sl != 0xFFFFu) { keys[sl] = kEmpty; acc[sl] = 0; inter[sl >> 1] = 0; }   // both halves are ours to clear
     }
     if (tid == 0) { keys[s_self] = kEmpty; acc[s_self] = 0; inter[s_self >> 1] = 0; acc[S] = 0; inter[S / 2] = 0; }
+  }
+  if (tid == 0) {
+    tier_add(J.tiers, HGP_TIER_SCORE_NOINTER, n_nointer);
+    tier_add(J.tiers, HGP_TIER_SCORE_PACKED, n_packed);
+    tier_add(J.tiers, HGP_TIER_SCORE_SPLIT, n_split);
   }
 }
 

@@ -87,6 +87,11 @@ class CPins(ctypes.Structure):
                 ("part", vp), ("count", vp)]
 
 
+class CCedges(ctypes.Structure):
+    _fields_ = [("K", ctypes.c_uint32), ("pad_", ctypes.c_uint32), ("P", ctypes.c_uint64), ("eid", vp), ("fp", vp),
+                ("nsrc", vp), ("size", vp), ("off", vp), ("pins", vp)]
+
+
 ALLOC_FN = ctypes.CFUNCTYPE(vp, vp, ctypes.c_size_t, vp)
 FREE_FN = ctypes.CFUNCTYPE(None, vp, vp, ctypes.c_size_t, vp)
 
@@ -158,6 +163,19 @@ def lib():
                                               ctypes.c_uint64, ctypes.c_uint64, vp]
         L.hgp_best_prefix.argtypes = [vp, vp, vp, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32),
                                       ctypes.POINTER(ctypes.c_int64)]
+        L.hgp_gamma.argtypes = [vp, vp, ctypes.c_uint32, vp, ctypes.POINTER(ctypes.c_uint32)]
+        L.hgp_coarse_bounds.argtypes = [vp, vp, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint32,
+                                        ctypes.POINTER(ctypes.c_uint32)]
+        L.hgp_contract_edges.argtypes = [vp, ctypes.POINTER(CCsr), vp, ctypes.c_uint32, ctypes.c_uint32,
+                                         ctypes.POINTER(CCedges)]
+        L.hgp_cedges_free.argtypes = [vp, ctypes.POINTER(CCedges)]
+        L.hgp_contract_merge.argtypes = [vp, ctypes.POINTER(CCsr), vp, vp, ctypes.POINTER(CCedges), ctypes.POINTER(CCsr)]
+        L.hgp_coarse_neighbors.argtypes = [vp, vp, vp, ctypes.c_uint32, vp, vp, vp, ctypes.c_uint32, ctypes.c_uint32,
+                                           ctypes.POINTER(CNbrs)]
+        for f in (L.hgp_gamma, L.hgp_coarse_bounds, L.hgp_contract_edges, L.hgp_contract_merge, L.hgp_coarse_neighbors):
+            f.restype = S
+        L.hgp_tier_counts.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+        L.hgp_tier_counts.restype = S
         for f in (L.hgp_pins_matrix, L.hgp_partition_metrics, L.hgp_propose_moves, L.hgp_in_sequence_gains,
                   L.hgp_sequence_violations, L.hgp_best_prefix):
             f.restype = S
@@ -282,6 +300,16 @@ class Ctx:
                 name, ms, n = item.rsplit(":", 2)
                 out[name] = (float(ms), int(n))
         return out
+
+    TIERS = ["fused_S", "fused_A", "fused_M", "fused_B", "nbrs_1", "nbrs_2", "nbrs_3", "score_nointer",
+             "score_packed", "score_split", "score_B", "score_W", "score_H", "cnbrs_A", "cnbrs_M", "cnbrs_B",
+             "cnbrs_C", "jump"]
+
+    def tier_counts(self, reset: bool = False) -> dict:
+        """hgp_tier_counts: nodes processed per kernel tier (include/hgp.h HGP_TIER_*)."""
+        arr = (ctypes.c_uint64 * 24)()
+        _check(lib().hgp_tier_counts(self.h, arr, int(reset)))
+        return {name: int(arr[i]) for i, name in enumerate(self.TIERS)}
 
     def copy(self, dst_ptr: int, src_ptr: int, nbytes: int):
         _check(lib().hgp_copy(self.h, vp(dst_ptr), vp(src_ptr), nbytes))
@@ -563,3 +591,76 @@ def best_prefix(ctx: Ctx, gain_seq: torch.Tensor, violations: torch.Tensor):
     _check(lib().hgp_best_prefix(ctx.h, _ptr(gain_seq), _ptr(violations), gain_seq.numel(), ctypes.byref(k),
                                  ctypes.byref(b)))
     return int(k.value), int(b.value)
+
+
+# ---- a5 in pieces for node/edge-range shards (include/hgp.h) ----------------------
+
+class Cedges:
+    """Pre-merge coarse edges of a fine edge range (library-owned; hgp_cedges_free)."""
+
+    def __init__(self, ctx: Ctx, c: CCedges):
+        self.ctx, self.c = ctx, c
+
+    K = property(lambda s: s.c.K)
+    P = property(lambda s: s.c.P)
+
+    def tensors(self) -> dict:
+        c = self.c
+        return {"eid": dev_view(c.eid, c.K, "u32", self), "fp": dev_view(c.fp, c.K, "u64", self),
+                "nsrc": dev_view(c.nsrc, c.K, "u32", self), "size": dev_view(c.size, c.K, "u32", self),
+                "off": dev_view(c.off, c.K + 1, "u64", self), "pins": dev_view(c.pins, c.P, "u32", self)}
+
+    def free(self):
+        if self.c is not None and self.ctx.h:
+            lib().hgp_cedges_free(self.ctx.h, ctypes.byref(self.c))
+        self.c = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class CedgesView:
+    """hgp_cedges over torch-owned device tensors (e.g. the all-gathered ranges)."""
+
+    def __init__(self, eid, fp, nsrc, size, off, pins):
+        self.t = [x.contiguous() for x in (eid, fp, nsrc, size, off, pins)]
+        K = self.t[0].numel()
+        self.c = CCedges(K, 0, self.t[5].numel(), *[vp(x.data_ptr()) for x in self.t])
+
+
+def gamma(ctx: Ctx, match_t: torch.Tensor, N: int, out: torch.Tensor) -> int:
+    """hgp_gamma: coarse ids of a symmetric match into out (u32 [N]); returns N'."""
+    nc = ctypes.c_uint32()
+    _check(lib().hgp_gamma(ctx.h, _ptr(match_t), N, _ptr(out), ctypes.byref(nc)))
+    return nc.value
+
+
+def coarse_bounds(ctx: Ctx, match_t: torch.Tensor, N: int, bounds: list[int]) -> list[int]:
+    arr_in = (ctypes.c_uint32 * len(bounds))(*bounds)
+    arr_out = (ctypes.c_uint32 * len(bounds))()
+    _check(lib().hgp_coarse_bounds(ctx.h, _ptr(match_t), N, arr_in, len(bounds), arr_out))
+    return list(arr_out)
+
+
+def contract_edges(ctx: Ctx, g: Csr, gamma_t: torch.Tensor, elo: int, ehi: int) -> Cedges:
+    out = CCedges()
+    _check(lib().hgp_contract_edges(ctx.h, ctypes.byref(g.c), _ptr(gamma_t), elo, ehi, ctypes.byref(out)))
+    return Cedges(ctx, out)
+
+
+def contract_merge(ctx: Ctx, g: Csr, match_t: torch.Tensor, gamma_t: torch.Tensor, allv: CedgesView) -> Csr:
+    out = CCsr()
+    _check(lib().hgp_contract_merge(ctx.h, ctypes.byref(g.c), _ptr(match_t), _ptr(gamma_t), ctypes.byref(allv.c),
+                                    ctypes.byref(out)))
+    return Csr(ctx, out)
+
+
+def coarse_neighbors(ctx: Ctx, match_t: torch.Tensor, gamma_t: torch.Tensor, N: int, seg_start: torch.Tensor,
+                     seg_len: torch.Tensor, nbr: torch.Tensor, clo: int, chi: int) -> Nbrs:
+    out = CNbrs()
+    _check(lib().hgp_coarse_neighbors(ctx.h, _ptr(match_t), _ptr(gamma_t), N, _ptr(seg_start), _ptr(seg_len), _ptr(nbr),
+                                      clo, chi, ctypes.byref(out)))
+    return Nbrs(ctx, out)

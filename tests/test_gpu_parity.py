@@ -219,7 +219,9 @@ def test_long_chain_pointer_jumping(hgp, ctx):
     n = 3000
     off = np.arange(0, 2 * n + 1, 2, dtype=np.uint64)
     pins = np.stack([np.arange(n), np.arange(1, n + 1)], axis=1).reshape(-1).astype(np.uint32)
-    hg = hgpgen.Hypergraph(n + 1, off, np.zeros(n, dtype=np.uint32), pins, np.ones(n, dtype=np.uint32),
+    # weights increasing along the path keep every child's gain > 0 (Eqs.9-10), so the best-child
+    # chain is the whole path (with equal weights the gains alternate to 0 and chains stay short)
+    hg = hgpgen.Hypergraph(n + 1, off, np.zeros(n, dtype=np.uint32), pins, np.arange(1, n + 1, dtype=np.uint32),
                            np.ones(n + 1, dtype=np.uint32))
     g = gpu_build(hgp, ctx, hg)
     nb = hgp.unique_neighbors(ctx, g)
@@ -233,6 +235,7 @@ def test_long_chain_pointer_jumping(hgp, ctx):
     hgp.match(ctx, cand, g.N, 4, m, None)
     rm, _, _ = ref.match(rcand, 4)
     assert np.array_equal(m.cpu().numpy(), rm)
+    assert ctx.tier_counts()["jump"] > 0, "the chain must reach a4's pointer-jumping fallback"
 
 
 FUSED_CASES = [
