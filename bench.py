@@ -35,6 +35,11 @@ import time
 
 import numpy as np
 
+# Library arrays come from torch's caching allocator; expandable segments keep the level's
+# tens-of-GB buffers (C5: the 2^34-entry neighbour pool, the coarse-neighbour bound pool) from
+# fragmenting its cache across steps.
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -296,6 +301,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-refine", action="store_true", help="skip the f1 quality / f3-f4 refinement-step leg")
+    ap.add_argument("--no-hier", action="store_true", help="skip the whole-hierarchy leg (implies --no-refine)")
     ap.add_argument("--dominant", default=None, help="kernel name for the roofline (default: measured top kernel)")
     args = ap.parse_args()
 
@@ -428,7 +434,9 @@ def main():
     # ---- whole hierarchy: a1 + hgp_coarsen to the stop rule, 1 GPU, CUDA events
     hier = None
     refine = None
-    if world == 1:
+    if args.no_hier:
+        pass
+    elif world == 1:
         def hierarchy(keep=False):
             g = hgp.build_csr(ctx, N, dev["edge_off"], dev["edge_nsrc"], dev["pins"], dev["edge_w"], dev["node_w"])
             rho, cg, cnb, levels = hgp.coarsen(ctx, g, params)
@@ -546,6 +554,14 @@ def main():
         t = oracle_level_seconds(hs, om, de, pi, hgpgen.default_noise_cap(hs), args.seed)
         line["cpu_baseline"] = {"value": hs.num_pins / t, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "sample": desc, "seconds": t, "host_cores": os.cpu_count()}
+        gold = os.path.join(ROOT, "tests", "golden", f"{args.workload}_s{args.seed}.json")
+        if os.path.exists(gold):   # the oracle on the FULL input (tools/golden_full.py; recorded, not re-run)
+            gd = json.load(open(gold))
+            if "oracle_seconds" in gd:
+                line["cpu_baseline"]["full_input"] = {
+                    "value": gd["oracle_pins_per_s"], "unit": UNIT, "seconds": gd["oracle_seconds"]["total"],
+                    "cores": gd.get("oracle_host", {}).get("cores_used", 1),
+                    "where": "build container, tools/golden_full.py (recorded)", "per_step_s": gd["oracle_seconds"]}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

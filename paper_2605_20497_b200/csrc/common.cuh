@@ -215,6 +215,13 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
+// A key probe that races with other threads' CAS inserts on purpose (the value is only a hint; the
+// CAS decides): a relaxed CTA-scope load says so to the memory model (same LDS in SASS).
+__device__ __forceinline__ uint32_t lds_hint_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.relaxed.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ void red_add_u32(uint32_t a, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }

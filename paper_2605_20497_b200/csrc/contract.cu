@@ -231,7 +231,15 @@ struct CNbrJob {
   unsigned long long *tiers;   // work counters (hgp_tier_counts)
   int tier;
   uint32_t cbase;              // coarse id of local coarse node 0 (a range of coarse nodes)
-};
+  uint32_t *nbr_w;             // in place (pool == nullptr): N'(c) overwrites N(a)'s then N(b)'s
+};                             // segment, which only c's CTA reads (each fine node has one c)
+
+// Where entry pos of N'(c) goes: the oversized pool slot, or in place over N(a) ‖ N(b).
+__device__ __forceinline__ uint32_t *cnbr_out(const CNbrJob &J, uint64_t base, uint64_t a0, uint64_t na, uint64_t b0,
+                                              uint64_t pos) {
+  if (J.pool) return J.pool + base + pos;
+  return J.nbr_w + (pos < na ? a0 + pos : b0 + (pos - na));
+}
 
 // insert key with an OR-ed flag kept in bit 31 of the slot (ids < 2^31 - 1, kEmpty masks to
 // 0x7FFFFFFF which is never an id); returns true if this call inserted the key.
@@ -263,14 +271,22 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
   extern __shared__ uint32_t dyn[];
   constexpr uint32_t NW = THREADS / 32;
   __shared__ uint32_t s_wcnt[NW];
+  __shared__ uint32_t s_n, s_out;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t log2s = J.log2s, S = 1u << log2s;
   uint32_t *keys = SMEM ? dyn : J.gtab + ((size_t)blockIdx.x << log2s);
+  uint16_t *slist = reinterpret_cast<uint16_t *>(dyn + S);          // SMEM: slots inserted (<= S/2)
   const uint32_t keys_s = SMEM ? opaque_u32(smem_u32addr(keys)) : 0u;
-  const uint32_t hmask = S - 1;
+  const uint32_t hmask = S - 1, lt = (1u << lane) - 1;
   const uint32_t total = J.list_count ? *J.list_count : J.Nc;
   uint64_t purged = 0;
   uint32_t done = 0;
+  if (SMEM) {   // cleared once; afterwards every node leaves exactly the slots it used to clear
+    for (uint32_t i = tid; i < S / 4; i += THREADS)
+      reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    if (tid == 0) { s_n = 0; s_out = 0; }
+    __syncthreads();
+  }
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t c = J.list ? J.list[t] : t;
     const uint32_t a = J.mem0[c], b = J.mem1[c];
@@ -284,9 +300,11 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
     }
     const uint64_t na = a1 - a0, nbn = b1 - b0;
     if (!J.list && na + nbn > J.cap) continue;                      // larger tier (uniform)
-    for (uint32_t i = tid; i < S / 4; i += THREADS)
-      reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-    __syncthreads();
+    if (!SMEM) {
+      for (uint32_t i = tid; i < S / 4; i += THREADS)
+        reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+      __syncthreads();
+    }
     // 4 entries per thread in flight: nbr loads, then the gamma gathers, then the inserts
     for (uint64_t k0 = tid; k0 < na + nbn; k0 += 4 * THREADS) {
       uint32_t v[4], gm[4];
@@ -304,18 +322,18 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
         purged += fl;
         if constexpr (SMEM) {
           uint32_t slot = hash_slot(gm[u], log2s);
-          uint32_t k = lds_u32(keys_s + 4 * slot);
+          uint32_t k = lds_hint_u32(keys_s + 4 * slot);
           while (true) {
             if (k == kEmpty) {
               k = cas_u32(keys_s + 4 * slot, kEmpty, fl ? (gm[u] | kPurge) : gm[u]);
-              if (k == kEmpty) break;
+              if (k == kEmpty) { slist[atomicAdd(&s_n, 1u)] = (uint16_t)slot; break; }   // a new key
             }
             if ((k & kIdMask) == gm[u]) {
               if (fl && !(k & kPurge)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(keys_s + 4 * slot), "r"(kPurge) : "memory");
               break;
             }
             slot = (slot + 1) & hmask;
-            k = lds_u32(keys_s + 4 * slot);
+            k = lds_hint_u32(keys_s + 4 * slot);
           }
         } else {
           uint32_t slot;
@@ -324,27 +342,49 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
       }
     }
     __syncthreads();
-    // compact: unflagged keys != c
-    const uint32_t per_w = S / NW, w0 = w * per_w, lt = (1u << lane) - 1;
-    uint32_t mine = 0;
-    for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
-      const uint32_t k = keys[sb + lane];
-      mine += __popc(__ballot_sync(0xFFFFFFFFu, !(k & kPurge) && k != c + J.cbase));   // kEmpty has bit 31 set
+    const uint64_t base = J.pool ? J.bound_off[c] : 0;
+    if constexpr (SMEM) {
+      // the inserted slots: unflagged keys other than c go to the pool (warp chunks claim their
+      // output positions with one shared atomic; the segment is a set), every slot is cleared
+      const uint32_t nl = s_n;
+      for (uint32_t i0 = w * 32; i0 < nl; i0 += THREADS) {
+        const uint32_t i = i0 + lane;
+        const bool valid = i < nl;
+        const uint32_t slot = valid ? slist[i] : 0u;
+        const uint32_t k = valid ? keys[slot] : kEmpty;
+        const bool keep = valid && !(k & kPurge) && k != c + J.cbase;   // kEmpty has bit 31 set
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+        uint32_t wpos = 0;
+        if (lane == 0 && bal) wpos = atomicAdd(&s_out, (uint32_t)__popc(bal));
+        wpos = __shfl_sync(0xFFFFFFFFu, wpos, 0);
+        if (keep) *cnbr_out(J, base, a0, na, b0, wpos + __popc(bal & lt)) = k;
+        if (valid) keys[slot] = kEmpty;
+      }
+      __syncthreads();
+      if (tid == 0) { J.cnt[c] = s_out; ++done; s_n = 0; s_out = 0; }
+      __syncthreads();
+    } else {
+      // global tables: unflagged keys != c by two ballot sweeps over the table
+      const uint32_t per_w = S / NW, w0 = w * per_w;
+      uint32_t mine = 0;
+      for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
+        const uint32_t k = keys[sb + lane];
+        mine += __popc(__ballot_sync(0xFFFFFFFFu, !(k & kPurge) && k != c + J.cbase));   // kEmpty has bit 31 set
+      }
+      if (lane == 0) s_wcnt[w] = mine;
+      __syncthreads();
+      uint32_t wpos = 0, tot = 0;
+      for (uint32_t q = 0; q < NW; ++q) { const uint32_t x = s_wcnt[q]; if (q < w) wpos += x; tot += x; }
+      for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
+        const uint32_t k = keys[sb + lane];
+        const bool keep = !(k & kPurge) && k != c + J.cbase;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+        if (keep) *cnbr_out(J, base, a0, na, b0, wpos + __popc(bal & lt)) = k;
+        wpos += __popc(bal);
+      }
+      if (tid == 0) { J.cnt[c] = tot; ++done; }
+      __syncthreads();
     }
-    if (lane == 0) s_wcnt[w] = mine;
-    __syncthreads();
-    uint32_t wpos = 0, tot = 0;
-    for (uint32_t q = 0; q < NW; ++q) { const uint32_t x = s_wcnt[q]; if (q < w) wpos += x; tot += x; }
-    const uint64_t base = J.bound_off[c];
-    for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
-      const uint32_t k = keys[sb + lane];
-      const bool keep = !(k & kPurge) && k != c + J.cbase;
-      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
-      if (keep) J.pool[base + wpos + __popc(bal & lt)] = k;
-      wpos += __popc(bal);
-    }
-    if (tid == 0) { J.cnt[c] = tot; ++done; }
-    __syncthreads();
   }
   if (tid == 0) tier_add(J.tiers, J.tier, done);
   purged = warp_sum(purged);
@@ -387,6 +427,22 @@ __global__ void k_cnbr_pack(const uint32_t *pool, const uint64_t *bound_off, con
     const uint32_t *src = pool + bound_off[c];
     uint32_t *dst = nbr + off[c];
     for (uint32_t i = lane; i < n; i += 32) dst[i] = src[i];
+    mx = max(mx, n);
+  }
+  mx = warp_max(mx);
+  if (lane == 0) atomicMax(maxdeg, mx);
+}
+
+// in place: N'(c) is the first cnt[c] entries of N(a)'s segment followed by N(b)'s
+__global__ void k_cnbr_pack_inplace(CNbrJob J, const uint64_t *off, uint32_t Nc, uint32_t *nbr, unsigned int *maxdeg) {
+  const uint32_t lane = lane_id();
+  uint32_t mx = 0;
+  for (uint32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < Nc; c += gridDim.x * (blockDim.x >> 5)) {
+    const uint32_t n = J.cnt[c], a = J.mem0[c], b = J.mem1[c];
+    const uint64_t a0 = J.nb_start[a], na = J.nb_len[a];
+    const uint64_t b0 = b == kNone ? 0 : J.nb_start[b];
+    uint32_t *dst = nbr + off[c];
+    for (uint32_t i = lane; i < n; i += 32) dst[i] = J.nbr_w[i < na ? a0 + i : b0 + (i - na)];
     mx = max(mx, n);
   }
   mx = warp_max(mx);
@@ -570,7 +626,8 @@ static hgp_status merge_impl(hgp_ctx *c, const hgp_csr *g, MergeJob M, hgp_csr *
 
 // Coarse neighbours (reading #7, #16) of the coarse nodes [clo, chi): member
 // segments are read through J's view (nb_off or nb_start/nb_len over nbr).
-static hgp_status cnbrs_impl(hgp_ctx *c, CNbrJob J, uint32_t clo, uint32_t chi, hgp_nbrs *CN, uint64_t *purged_out) {
+static hgp_status cnbrs_impl(hgp_ctx *c, CNbrJob J, uint32_t clo, uint32_t chi, hgp_nbrs *CN, uint64_t *purged_out,
+                             bool inplace = false) {
   hgp_status st = HGP_OK;
   const uint32_t Nc = chi - clo;
   // the kernels index coarse nodes from 0: shift the member arrays
@@ -580,7 +637,9 @@ static hgp_status cnbrs_impl(hgp_ctx *c, CNbrJob J, uint32_t clo, uint32_t chi, 
   if (st) return st;
   uint64_t Vb = 0;
   HGP_TRY(scan_exclusive(c, BoundIn{J.mem0, J.mem1, J.nb_off, J.nb_off ? nullptr : J.nb_len}, Nc, bound_off, &Vb));
-  uint32_t *pool = scratch_raw<uint32_t>(c, Vb, &st);
+  // in place (the level-0 pool view, consumed by this call): no bound pool — N'(c) overwrites the
+  // segments of its members (C5: saves V entries, ~40 GB)
+  uint32_t *pool = inplace ? nullptr : scratch_raw<uint32_t>(c, Vb, &st);
   uint32_t *ccnt = scratch_raw<uint32_t>(c, Nc, &st);
   uint32_t *lists = scratch_raw<uint32_t>(c, 3 * (size_t)Nc, &st);
   uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
@@ -589,31 +648,32 @@ static hgp_status cnbrs_impl(hgp_ctx *c, CNbrJob J, uint32_t clo, uint32_t chi, 
   if (st) return st;
   static uint64_t attr_dev = 0;   // per device: cudaFuncSetAttribute applies to the current one
   if (once_per_device(&attr_dev, c->device)) {
-    cudaFuncSetAttribute(k_coarse_nbrs<kCAThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kCALog);
+    cudaFuncSetAttribute(k_coarse_nbrs<kCAThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 5 << kCALog);
     // tiers M and B share the instantiation <256, true>: the attribute is the larger table's
     static_assert(kCMThreads == kCBThreads && kCMLog < kCBLog, "M and B share one instantiation");
-    cudaFuncSetAttribute(k_coarse_nbrs<kCBThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kCBLog);
+    cudaFuncSetAttribute(k_coarse_nbrs<kCBThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 5 << kCBLog);
   }
   J.bound_off = bound_off;
   J.pool = pool; J.cnt = ccnt; J.Nc = Nc; J.purged = misc; J.tiers = c->d_tiers; J.tier = HGP_TIER_CNBRS_A;
+  J.nbr_w = inplace ? const_cast<uint32_t *>(J.nbr) : nullptr;
   J.cbase = clo;
   const uint32_t capA = 1u << (kCALog - 1), capM = 1u << (kCMLog - 1), capB = 1u << (kCBLog - 1);
   J.list = nullptr; J.list_count = nullptr; J.cap = capA; J.log2s = kCALog;
   const uint32_t gA = Nc < 64u * c->sm_count ? (Nc ? Nc : 1) : 64u * c->sm_count;
-  if (Nc) HGP_TRY(launch(c, "coarse_nbrs_A", k_coarse_nbrs<kCAThreads, true>, dim3(gA), dim3(kCAThreads), 4u << kCALog, J));
+  if (Nc) HGP_TRY(launch(c, "coarse_nbrs_A", k_coarse_nbrs<kCAThreads, true>, dim3(gA), dim3(kCAThreads), 5u << kCALog, J));
   if (Nc) HGP_TRY(launch(c, "cnbr_classify", k_cnbr_classify, dim3(grid_n(c, Nc)), dim3(256), 0, (const uint64_t *)bound_off,
                          Nc, capA, capM, capB, lists, lists + Nc, lists + 2 * (size_t)Nc, counts, misc + 1));
   uint32_t hc[3];
   HGP_TRY(read_back(c, counts, 12, hc));
   if (hc[0]) {
     J.list = lists; J.list_count = counts; J.cap = capM; J.log2s = kCMLog; J.tier = HGP_TIER_CNBRS_M;
-    HGP_TRY(launch(c, "coarse_nbrs_M", k_coarse_nbrs<kCMThreads, true>, dim3(3 * c->sm_count), dim3(kCMThreads),
-                   4u << kCMLog, J));
+    HGP_TRY(launch(c, "coarse_nbrs_M", k_coarse_nbrs<kCMThreads, true>, dim3(2 * c->sm_count), dim3(kCMThreads),
+                   5u << kCMLog, J));
   }
   if (hc[1]) {
     J.list = lists + Nc; J.list_count = counts + 1; J.cap = capB; J.log2s = kCBLog; J.tier = HGP_TIER_CNBRS_B;
     HGP_TRY(launch(c, "coarse_nbrs_B", k_coarse_nbrs<kCBThreads, true>, dim3(c->sm_count), dim3(kCBThreads),
-                   4u << kCBLog, J));
+                   5u << kCBLog, J));
   }
   if (hc[2]) {
     uint64_t mb = 0;
@@ -636,9 +696,12 @@ static hgp_status cnbrs_impl(hgp_ctx *c, CNbrJob J, uint32_t clo, uint32_t chi, 
   CN->V = Vc;
   CN->nbr = dalloc_n<uint32_t>(c, Vc, &st);
   if (st) return st;
-  if (Nc)
+  if (Nc && !inplace)
     HGP_TRY(launch(c, "cnbr_pack", k_cnbr_pack, dim3(grid_n(c, Nc, 8)), dim3(256), 0, (const uint32_t *)pool,
                    (const uint64_t *)bound_off, (const uint32_t *)ccnt, (const uint64_t *)CN->off, Nc, CN->nbr, maxes));
+  if (Nc && inplace)
+    HGP_TRY(launch(c, "cnbr_pack", k_cnbr_pack_inplace, dim3(grid_n(c, Nc, 8)), dim3(256), 0, J,
+                   (const uint64_t *)CN->off, Nc, CN->nbr, maxes));
   uint32_t hmax[2];
   HGP_TRY(read_back(c, maxes, 8, hmax));
   CN->max_deg = hmax[0];
@@ -669,7 +732,7 @@ hgp_status contract_impl(hgp_ctx *c, const hgp_csr *g, const hgp_nbrs *nb, const
   J.nb_start = view ? view->start : nullptr; J.nb_len = view ? view->len : nullptr;
   J.nbr = view ? view->nbr : nb->nbr;
   uint64_t purged = 0;
-  HGP_TRY(cnbrs_impl(c, J, 0, Nc, CN, &purged));
+  HGP_TRY(cnbrs_impl(c, J, 0, Nc, CN, &purged, view != nullptr));
   if (stats) {
     // kept edges = classes' members; dropped = E - kept; merged = kept - Ec
     uint32_t *kc = scratch_zero<uint32_t>(c, 1, &st);

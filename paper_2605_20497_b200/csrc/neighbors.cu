@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) sl[u] = hash_slot(m[u], J.log2s);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) kk[u] = lds_u32(tab_s + 4 * sl[u]);
+          for (int u = 0; u < 4; ++u) kk[u] = lds_hint_u32(tab_s + 4 * sl[u]);
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (m[u] == n || kk[u] == m[u]) continue;
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
               }
               if (k2 == m[u]) break;
               slot = (slot + 1) & hmask;
-              k2 = lds_u32(tab_s + 4 * slot);
+              k2 = lds_hint_u32(tab_s + 4 * slot);
             }
           }
           }
