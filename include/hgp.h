@@ -197,6 +197,7 @@ enum {
   HGP_TIER_CNBRS_B = 15,     /* a5 coarse neighbours, 32768-slot table */
   HGP_TIER_CNBRS_C = 16,     /* a5 coarse neighbours, global-memory tables */
   HGP_TIER_JUMP = 17,        /* a4 pointer-jumping fallback (nodes of over-long best-child chains) */
+  HGP_TIER_FUSED_W = 18,     /* fused a2+a3, one warp per small node (<= 256 pin visits) */
   HGP_TIERS = 24
 };
 /* HOST out[HGP_TIERS] <- the counters (synchronises); reset != 0 zeroes them afterwards. */

@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
   uint32_t *keys = SMEM ? dyn : J.gtab + ((size_t)blockIdx.x << log2s);
   uint16_t *slist = reinterpret_cast<uint16_t *>(dyn + S);          // SMEM: slots inserted (<= S/2)
   const uint32_t keys_s = SMEM ? opaque_u32(smem_u32addr(keys)) : 0u;
-  const uint32_t hmask = S - 1, lt = (1u << lane) - 1;
+  const uint32_t lt = (1u << lane) - 1;
   const uint32_t total = J.list_count ? *J.list_count : J.Nc;
   uint64_t purged = 0;
   uint32_t done = 0;
@@ -300,8 +300,15 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
     }
     const uint64_t na = a1 - a0, nbn = b1 - b0;
     if (!J.list && na + nbn > J.cap) continue;                      // larger tier (uniform)
+    // global tables: only nextpow2(2 (|N(a)| + |N(b)| + 1)) slots of the CTA's region
+    uint32_t nlog = log2s;
     if (!SMEM) {
-      for (uint32_t i = tid; i < S / 4; i += THREADS)
+      nlog = 6;
+      while ((1ull << nlog) < 2 * (na + nbn + 1) && nlog < log2s) ++nlog;
+    }
+    const uint32_t Sn = 1u << nlog, nmask = Sn - 1;
+    if (!SMEM) {
+      for (uint32_t i = tid; i < Sn / 4; i += THREADS)
         reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
       __syncthreads();
     }
@@ -321,7 +328,7 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
         const bool fl = (v[u] & kPurge) != 0;
         purged += fl;
         if constexpr (SMEM) {
-          uint32_t slot = hash_slot(gm[u], log2s);
+          uint32_t slot = hash_slot(gm[u], nlog);
           uint32_t k = lds_hint_u32(keys_s + 4 * slot);
           while (true) {
             if (k == kEmpty) {
@@ -332,12 +339,12 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
               if (fl && !(k & kPurge)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(keys_s + 4 * slot), "r"(kPurge) : "memory");
               break;
             }
-            slot = (slot + 1) & hmask;
+            slot = (slot + 1) & nmask;
             k = lds_hint_u32(keys_s + 4 * slot);
           }
         } else {
           uint32_t slot;
-          hs_insert_flagged(keys, log2s, gm[u], fl, &slot);
+          hs_insert_flagged(keys, nlog, gm[u], fl, &slot);
         }
       }
     }
@@ -365,7 +372,7 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
       __syncthreads();
     } else {
       // global tables: unflagged keys != c by two ballot sweeps over the table
-      const uint32_t per_w = S / NW, w0 = w * per_w;
+      const uint32_t per_w = Sn / NW, w0 = w * per_w;
       uint32_t mine = 0;
       for (uint32_t sb = w0; sb < w0 + per_w; sb += 32) {
         const uint32_t k = keys[sb + lane];

@@ -605,6 +605,211 @@ __global__ void k_sample_lists(uint32_t lo, uint32_t nn, uint32_t stride, uint32
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Tier W: one WARP per small node (bound(n) = sum over I(n) of (|e| - 1) <= kWCap, so at most
+// kWCap neighbours): a private 512-slot table per warp, no CTA barriers, no 4096-slot sweeps —
+// the per-node fixed costs that dominate power-law inputs (C3/C4: most nodes have ~10-100 pin
+// visits) shrink to the warp's own work. Same integer sums and tie rules as the CTA tiers; nodes
+// it cannot represent (packed form inexact, scores >= 2^32, a probe run over the cap) are handed
+// to the CTA tiers through F.defer_list.
+constexpr uint32_t kWLog = 9, kWSlots = 1u << kWLog, kWCap = 256, kWWarps = 8;
+
+__global__ void k_small_split(FusedJob F, uint32_t lo, uint32_t nn, uint32_t *lw, uint32_t *cw, uint32_t *lr,
+                              uint32_t *cr) {
+  const ScoreJob &J = F.S;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
+    const uint32_t n = lo + i;
+    uint64_t b = 0;
+    for (uint64_t k = J.inc_off[n]; k < J.inc_off[n + 1] && b <= kWCap; ++k) {
+      const uint32_t e = J.inc[k];
+      b += J.edge_off[e + 1] - J.edge_off[e] - 1;
+    }
+    if (b <= kWCap) lw[atomicAdd(cw, 1u)] = n;
+    else lr[atomicAdd(cr, 1u)] = n;
+  }
+}
+
+template <int PIMAX>
+__global__ void __launch_bounds__(kWWarps * 32) k_nbrscore_w(FusedJob F) {
+  __shared__ __align__(16) uint32_t s_keys[kWWarps][kWSlots];
+  __shared__ __align__(16) uint32_t s_acc[kWWarps][kWSlots];
+  const ScoreJob &J = F.S;
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  constexpr uint32_t hmask = kWSlots - 1;
+  const uint32_t keys_s = opaque_u32(smem_u32addr(s_keys[w])), acc_s = opaque_u32(smem_u32addr(s_acc[w]));
+  uint32_t *keys = s_keys[w], *acc = s_acc[w];
+  for (uint32_t i = lane; i < kWSlots; i += 32) { keys[i] = kEmpty; acc[i] = 0; }
+  __syncwarp();
+  const uint32_t total = *F.list_count;
+  uint32_t done = 0;
+  for (uint32_t t = blockIdx.x * kWWarps + w; t < total; t += gridDim.x * kWWarps) {
+    const uint32_t n = F.list[t];
+    const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1], iin = i0 + J.inc_nin[n];
+    const uint32_t inn = J.in_mu[n];
+    // sum and gcd of c(e) over I(n): is the packed accumulator (eta/g << ib | inter) exact?
+    uint64_t sum = 0, gg = 0;
+    for (uint64_t k = i0 + lane; k < i1; k += 32) {
+      const uint64_t ce = F.cv[J.inc[k]];
+      sum += ce;
+      gg = gcd64(gg, ce);
+    }
+    sum = warp_sum(sum);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t og = __shfl_xor_sync(0xFFFFFFFFu, gg, o);
+      if (og != gg) gg = gcd64(gg, og);
+    }
+    const uint64_t g = gg ? gg : 1;
+    const uint32_t ib = inn ? 32 - __clz(inn) : 0;
+    const bool exact = (((unsigned __int128)(sum / g + 1)) << ib) <= ((unsigned __int128)1 << 32);
+    const bool small = (unsigned __int128)sum + J.noise_cap < ((unsigned __int128)1 << 32);
+    if (!exact || !small) {
+      if (lane == 0) F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
+      continue;
+    }
+    if (lane == 0) keys[hash_slot(n, kWLog)] = n;                 // self-visits land in n's slot
+    __syncwarp();
+    bool full = false;
+    // incident edges 32 at a time (lane = edge), their pins as one flat sequence over the lanes
+    for (uint64_t c0 = i0; c0 < i1; c0 += 32) {
+      const bool mine = c0 + lane < i1;
+      uint32_t len = 0, ns = 0, as = 0, ad = 0, a = 0;
+      if (mine) {
+        const uint32_t e = J.inc[c0 + lane];
+        const uint64_t ea = J.edge_off[e];
+        a = (uint32_t)ea;                                          // P < 2^32 on this path
+        len = (uint32_t)(J.edge_off[e + 1] - ea);
+        ns = J.edge_nsrc[e];
+        const uint64_t ce = F.cv[e];
+        as = (uint32_t)((ce == g ? 1ull : ce / g) << ib);
+        ad = as + (c0 + lane < iin ? J.edge_mu[e] : 0u);           // m in dst(e), e in in(n)
+      }
+      const uint32_t incl = warp_incl_scan(len);
+      const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      for (uint32_t f0 = 0; f0 < tot; f0 += 32) {
+        const uint32_t f = f0 + lane;
+        const bool val = f < tot;
+        // the edge holding flat position f: the first lane r with incl[r] > f (5 shuffles)
+        uint32_t r = 0;
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+          const uint32_t x = __shfl_sync(0xFFFFFFFFu, incl, r + st - 1);
+          if (x <= f) r += st;
+        }
+        const uint32_t rs = __shfl_sync(0xFFFFFFFFu, incl - len, r), ra = __shfl_sync(0xFFFFFFFFu, a, r);
+        const uint32_t rns = __shfl_sync(0xFFFFFFFFu, ns, r), ras = __shfl_sync(0xFFFFFFFFu, as, r);
+        const uint32_t rad = __shfl_sync(0xFFFFFFFFu, ad, r);
+        if (!val) continue;
+        const uint32_t j = f - rs;
+        const uint32_t m = __ldg(J.pins + ra + j);
+        const uint32_t add = j >= rns ? rad : ras;
+        uint32_t slot = hash_slot(m, kWLog), probes = 0;
+        while (true) {
+          uint32_t k = lds_u32(keys_s + 4 * slot);
+          if (k == kEmpty) {
+            k = cas_u32(keys_s + 4 * slot, kEmpty, m);
+            if (k == kEmpty) k = m;
+          }
+          if (k == m) { red_add_u32(acc_s + 4 * slot, add); break; }
+          if (++probes > kProbeCap) { full = true; break; }
+          slot = (slot + 1) & hmask;
+        }
+      }
+    }
+    __syncwarp();
+    if (__any_sync(0xFFFFFFFFu, full)) {                           // (cannot happen below 1/2 load)
+      for (uint32_t i = lane; i < kWSlots; i += 32) { keys[i] = kEmpty; acc[i] = 0; }
+      __syncwarp();
+      if (lane == 0) F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
+      continue;
+    }
+    // the occupied slots but n's: count, reserve N(n) in the pool, validity / flags / noise and the
+    // warp's top-Pi over 4 slots per lane per step; the table is cleared behind the sweep
+    uint32_t cnt = 0;
+#pragma unroll
+    for (uint32_t j = 4 * lane; j < kWSlots; j += 128) {
+      const uint4 k4 = lds_v4(keys_s + 4 * j);
+      cnt += (uint32_t)(k4.x != kEmpty && k4.x != n) + (uint32_t)(k4.y != kEmpty && k4.y != n) +
+             (uint32_t)(k4.z != kEmpty && k4.z != n) + (uint32_t)(k4.w != kEmpty && k4.w != n);
+    }
+    cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    unsigned long long st0 = 0;
+    if (lane == 0) st0 = atomicAdd(F.pool_cursor, (unsigned long long)cnt);
+    st0 = __shfl_sync(0xFFFFFFFFu, st0, 0);
+    const bool pool_ok = st0 + cnt <= F.pool_cap;
+    if (lane == 0) {
+      F.cnt[n - J.lo] = cnt;
+      if (pool_ok) F.start[n - J.lo] = st0 + F.start_bias;
+      else F.pool_list[atomicAdd(F.pool_count, 1u)] = n;
+    }
+    const EvalCtx E = eval_ctx(J, n, ib);
+    const uint32_t g32 = (uint32_t)g, cap32 = (uint32_t)J.noise_cap;
+    uint64_t carry = 0;
+    uint32_t pos = 0;
+#pragma unroll
+    for (uint32_t j = 4 * lane; j < kWSlots; j += 128) {
+      const uint4 k4 = lds_v4(keys_s + 4 * j);
+      const uint4 a4 = lds_v4(acc_s + 4 * j);
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(keys_s + 4 * j), "r"(kEmpty) : "memory");
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(acc_s + 4 * j), "r"(0u) : "memory");
+      const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w}, aa[4] = {a4.x, a4.y, a4.z, a4.w};
+      bool occ[4];
+      uint32_t c = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { occ[u] = kk[u] != kEmpty && kk[u] != n; c += occ[u]; }
+      const uint32_t incl = warp_incl_scan(c);
+      uint32_t p = pos + incl - c;
+      uint64_t key[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        key[u] = 0;
+        if (!occ[u] || !pool_ok) continue;
+        uint32_t cn;
+        if (eval_one(F, E, make_uint2(kk[u], aa[u]), st0 + p, cn)) {
+          uint32_t s32 = cn * g32;                                 // eta(n, m) < 2^32
+          if (cap32) {
+            const uint64_t hk = ((uint64_t)min(n, kk[u]) << 32) | max(n, kk[u]);
+            s32 += (uint32_t)__umul64hi(splitmix64(hk ^ J.seed_mix), J.noise_cap + 1);   // uniform in [0, cap]
+          }
+          key[u] = ((uint64_t)s32 << 32) | kk[u];
+        }
+        ++p;
+      }
+      pos += __shfl_sync(0xFFFFFFFFu, incl, 31);
+      uint64_t nc = 0;
+      for (uint32_t rr = 0; rr < J.pi; ++rr) {                      // the warp's pi best so far
+        uint64_t lm = carry;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) lm = key[u] > lm ? key[u] : lm;
+        const uint32_t hi = (uint32_t)(lm >> 32);
+        const uint32_t mhi = __reduce_max_sync(0xFFFFFFFFu, hi);
+        if (mhi == 0) break;
+        const uint32_t mlo = __reduce_max_sync(0xFFFFFFFFu, hi == mhi ? (uint32_t)lm : 0u);
+        const uint64_t K = ((uint64_t)mhi << 32) | mlo;
+        if (carry == K) carry = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (key[u] == K) key[u] = 0;
+        if (lane == rr) nc = K;
+      }
+      carry = nc;
+    }
+    __syncwarp();
+    if (pool_ok) {
+      for (uint32_t rr = lane; rr < J.pi; rr += 32) {
+        hgp_cand cd;
+        cd.score = carry >> 32;
+        cd.id = carry ? (uint32_t)carry : kNone;
+        cd.pad = 0;
+        J.cand[(uint64_t)n * J.pi + rr] = cd;
+      }
+      if (lane == 0) ++done;
+    }
+  }
+  if (lane == 0) tier_add(F.tiers, HGP_TIER_FUSED_W, done);
+}
+
 // tiers of the fused kernel: A 4096 slots (40 KB incl. the dense list) for every node, M 8192
 // slots (72 KB, 3 CTAs/SM), B 16384 slots (144 KB, 1 CTA/SM); what B cannot hold (or the packed
 // accumulator cannot represent) goes to the unfused kernels.
@@ -616,6 +821,7 @@ struct TierLists {
   uint32_t hn;                          // host upper bound of the input count (grid sizing)
   uint32_t *la, *ca, *lm, *cm;          // A -> M, M -> B hand-off
   uint32_t *ld, *cd;                    // B -> unfused (appended)
+  bool small_first;                     // route small nodes to tier W first (range input only)
 };
 
 
@@ -633,6 +839,22 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
   const uint32_t per_sm = MINB;                                     // exactly the resident CTAs
   const uint32_t gA = L.hn < per_sm * sm ? L.hn : per_sm * sm;
   if (gA == 0) return HGP_OK;
+  if (!L.in_list && L.small_first) {
+    // tier W first: nodes with <= kWCap pin visits, one warp each; the rest (and W's deferrals)
+    // continue below as a list
+    hgp_status st = HGP_OK;
+    uint32_t *lw = scratch_raw<uint32_t>(c, L.hn, &st), *lr = scratch_raw<uint32_t>(c, L.hn, &st);
+    uint32_t *cnt2 = scratch_zero<uint32_t>(c, 2, &st);
+    if (st) return st;
+    HGP_TRY(launch(c, "small_split", k_small_split, dim3(div_up(L.hn, 256) < 4096 ? div_up(L.hn, 256) : 4096), dim3(256),
+                   0, F, F.S.lo, L.hn, lw, cnt2, lr, cnt2 + 1));
+    FusedJob FW = F;
+    FW.list = lw; FW.list_count = cnt2; FW.defer_list = lr; FW.defer_count = cnt2 + 1;
+    HGP_TRY(launch(c, "nbrscore_W", k_nbrscore_w<PIMAX>, dim3(16 * sm), dim3(kWWarps * 32), 0, FW));
+    TierLists L2 = L;
+    L2.in_list = lr; L2.in_count = cnt2 + 1; L2.small_first = false;
+    return fused_tiers_t<PIMAX, TA, MINB>(c, F, L2);
+  }
   constexpr uint32_t kStride = 64;
   const uint64_t sample_min = c->opt.fused_sample_min;            // 1024 * kStride by default
   if (!L.in_list && L.hn >= sample_min && L.hn >= 2 * kStride) {
@@ -754,7 +976,8 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   F.tiers = c->d_tiers;
   F.pool = pool; F.pool_cap = pool_cap; F.pool_cursor = misc + 1; F.start = start; F.cnt = cnt;
   F.pool_list = LP; F.pool_count = counts + 3;
-  TierLists L{nullptr, nullptr, nn, LA, counts + 0, LM, counts + 1, LD, counts + 2};
+  // power-law inputs (few pins per node on average) are mostly small nodes: warp-per-node tier first
+  TierLists L{nullptr, nullptr, nn, LA, counts + 0, LM, counts + 1, LD, counts + 2, g->P <= 32ull * g->N};
   if (all_unfused) HGP_TRY(launch(c, "iota", k_iota, dim3(div_up(nn, 256) < 4096 ? div_up(nn, 256) : 4096), dim3(256), 0,
                                   LD, counts + 2, lo, nn));
   else if (p->pi <= 4) HGP_TRY(fused_tiers<4>(c, F, L));
@@ -772,7 +995,7 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
     F2.pool = pool2; F2.pool_cap = need ? need : 1; F2.pool_cursor = misc + 2;
     F2.start_bias = (uint64_t)(pool2 - pool);
     F2.pool_list = LA; F2.pool_count = counts + 6;
-    TierLists L2{LP, counts + 3, hc[3], LA, counts + 4, LM, counts + 5, LD, counts + 2};
+    TierLists L2{LP, counts + 3, hc[3], LA, counts + 4, LM, counts + 5, LD, counts + 2, false};
     if (p->pi <= 4) HGP_TRY(fused_tiers<4>(c, F2, L2));
     else HGP_TRY(fused_tiers<16>(c, F2, L2));
     HGP_TRY(read_back(c, counts, sizeof(hc), hc));

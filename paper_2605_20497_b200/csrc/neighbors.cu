@@ -42,20 +42,39 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
   __shared__ unsigned long long s_start;
   constexpr uint32_t NW = THREADS / 32;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint32_t S = 1u << J.log2s;
   uint32_t *tab = SMEM ? dyn : J.gtab + ((size_t)blockIdx.x << J.log2s);
   const uint32_t total = J.list_count ? *J.list_count : J.nall;
   uint32_t done = 0;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = J.list ? J.list[t] : J.lo + t;
-    for (uint32_t i = tid; i < S / 4; i += THREADS)
+    // global tables: only nextpow2(2 (bound + 1) + margin) slots of the CTA's region, bound =
+    // sum over I(n) of (|e| - 1), so clearing and sweeping cost what the node needs
+    uint32_t nlog = J.log2s;
+    if (!SMEM) {
+      uint64_t bsum = 0;
+      for (uint64_t k = J.inc_off[n] + tid; k < J.inc_off[n + 1]; k += THREADS) {
+        const uint32_t e = J.inc[k];
+        bsum += J.edge_off[e + 1] - J.edge_off[e] - 1;
+      }
+      bsum = warp_sum(bsum);
+      if (tid == 0) s_start = 0;
+      __syncthreads();
+      if (lane == 0 && bsum) atomicAdd(&s_start, (unsigned long long)bsum);
+      __syncthreads();
+      const uint64_t need = 2 * (s_start + 1) + 128 * NW;
+      __syncthreads();                                             // s_start is reused below
+      nlog = 6;
+      while ((1ull << nlog) < need && nlog < J.log2s) ++nlog;
+    }
+    const uint32_t Sn = 1u << nlog;
+    for (uint32_t i = tid; i < Sn / 4; i += THREADS)
       reinterpret_cast<uint4 *>(tab)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     if (tid == 0) { s_cnt = 0; s_state = 0; }
     __syncthreads();
     const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1];
     volatile uint32_t *vcnt = &s_cnt;
     const uint32_t tab_s = SMEM ? opaque_u32(smem_u32addr(tab)) : 0u;
-    const uint32_t hmask = S - 1;
+    const uint32_t hmask = Sn - 1;
     bool stop = false;
     uint32_t nins = 0;                                             // new keys, flushed per block
     // a warp loads the offsets of 32 incident edges at once (lane = edge), then walks them with
@@ -89,11 +108,11 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
           if constexpr (!SMEM) {   // global-memory table: generic atomics
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-              if (m[u] != n && hs_insert(tab, J.log2s, m[u])) ++nins;
+              if (m[u] != n && hs_insert(tab, nlog, m[u])) ++nins;
           } else {
           uint32_t sl[4], kk[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) sl[u] = hash_slot(m[u], J.log2s);
+          for (int u = 0; u < 4; ++u) sl[u] = hash_slot(m[u], nlog);
 #pragma unroll
           for (int u = 0; u < 4; ++u) kk[u] = lds_hint_u32(tab_s + 4 * sl[u]);
 #pragma unroll
@@ -135,7 +154,7 @@ __global__ void __launch_bounds__(THREADS) k_nbrs(NbrJob J) {
       if (tid == 0) s_cnt = 0;
       __syncthreads();
       const uint32_t lt = (1u << lane) - 1;
-      for (uint32_t sb = w * 32; sb < S; sb += NW * 32) {
+      for (uint32_t sb = w * 32; sb < Sn; sb += NW * 32) {
         const uint32_t v = tab[sb + lane];
         const bool has = v != kEmpty;
         const uint32_t bal = __ballot_sync(0xFFFFFFFFu, has);

@@ -52,6 +52,14 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
       if (tid == 0) J.big_list[atomicAdd(J.big_count, 1u)] = n;
       continue;
     }
+    // table of this node: the tier's shared table, or (global tables) just nextpow2(2 (|N(n)| + 1))
+    // slots of the CTA's region, so clearing and probing cost what the node needs
+    uint32_t nlog = log2s;
+    if (!SMEM) {
+      nlog = 6;
+      while ((1ull << nlog) < 2 * (b1 - b0 + 1) + 2 && nlog < log2s) ++nlog;
+    }
+    const uint32_t Sn = 1u << nlog;
     const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1], iin = i0 + J.inc_nin[n];
     const uint32_t inn = J.in_mu[n];
     // ---- phase 0 (P32): gcd and sum of c(e) over I(n) decide whether the packed form is exact
@@ -108,28 +116,28 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
       }
     }
     // ---- phase 1: bins = unflagged neighbours (+ n itself in P32 mode: every self-visit then
-    // hits a real slot, no per-pin test; misses of purged neighbours go to a trash slot S)
-    for (uint32_t i = tid; i < S; i += THREADS) {
+    // hits a real slot, no per-pin test; misses of purged neighbours go to a trash slot Sn)
+    for (uint32_t i = tid; i < Sn; i += THREADS) {
       keys[i] = kEmpty;
       acc[i] = 0;
       if (MODE == kModeWide) eta[i] = 0;
       if (MODE == kModeSplit) inter32[i] = 0;
     }
-    if (MODE != kModeWide && tid == 0) acc[S] = 0;
-    if (MODE == kModeSplit && tid == 0) inter32[S] = 0;
+    if (MODE != kModeWide && tid == 0) acc[Sn] = 0;
+    if (MODE == kModeSplit && tid == 0) inter32[Sn] = 0;
     __syncthreads();
     for (uint64_t k = b0 + tid; k < b1; k += THREADS) {
       const uint32_t v = J.nbr[k];
-      if (!(v & kPurge)) hs_insert(keys, log2s, v);
+      if (!(v & kPurge)) hs_insert(keys, nlog, v);
     }
-    if (MODE != kModeWide && tid == 0) hs_insert(keys, log2s, n);
+    if (MODE != kModeWide && tid == 0) hs_insert(keys, nlog, n);
     __syncthreads();
     // ---- phase 2: traverse I(n): a warp loads the metadata of 32 incident edges at
     // once (lane = edge), then walks them; pins are fetched 128 at a time (4 per lane in flight).
     // Incident edges are dealt round-robin to warps (edge i0 + w + NW*l, l = 0, 1, ...): balanced.
     const uint32_t keys_s = opaque_u32(smem_u32addr(keys)), acc_s = opaque_u32(smem_u32addr(acc));
     const uint32_t inter_s = MODE == kModeSplit ? smem_u32addr(inter32) : 0u;
-    const uint32_t hmask = S - 1;
+    const uint32_t hmask = Sn - 1;
     for (uint64_t kb = i0 + w; kb < i1; kb += (uint64_t)NW * 32) {
       const uint64_t k = kb + (uint64_t)NW * lane;
       uint64_t a = 0, ce = 0;
@@ -177,7 +185,7 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
             // first probes of the 4 pins issued back to back (ILP), collisions resolved after
             uint32_t sl[4], kk[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) sl[u] = hash_slot(m[u], log2s);
+            for (int u = 0; u < 4; ++u) sl[u] = hash_slot(m[u], nlog);
 #pragma unroll
             for (int u = 0; u < 4; ++u) kk[u] = lds_u32(keys_s + 4 * sl[u]);
 #pragma unroll
@@ -187,7 +195,7 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
               if (kk[u] != m[u]) {
                 uint32_t k2 = kk[u];
                 while (true) {
-                  if (k2 == kEmpty) { slot = S; break; }               // purged neighbour -> trash
+                  if (k2 == kEmpty) { slot = Sn; break; }               // purged neighbour -> trash
                   slot = (slot + 1) & hmask;
                   k2 = lds_u32(keys_s + 4 * slot);
                   if (k2 == m[u]) break;
@@ -209,7 +217,7 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
             const bool dst = b4 + u * 32 + lane >= sj;
             {
               if (m[u] == n) continue;
-              const uint32_t slot = hs_find(keys, log2s, m[u]);
+              const uint32_t slot = hs_find(keys, nlog, m[u]);
               if (slot == kNone) continue;                          // purged neighbour
               atomicAdd(reinterpret_cast<unsigned long long *>(&eta[slot]), (unsigned long long)ce_j);
               if (dst && mu_j) atomicAdd(&acc[slot], mu_j);
@@ -228,7 +236,7 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
     for (uint64_t k = b0 + tid; k < b1; k += THREADS) {
       const uint32_t v = J.nbr[k];
       if (v & kPurge) continue;
-      const uint32_t slot = hs_find(keys, log2s, v);
+      const uint32_t slot = hs_find(keys, nlog, v);
       uint64_t e_nm, inter;
       if (MODE == kModeP32) {
         const uint32_t x = acc[slot];
