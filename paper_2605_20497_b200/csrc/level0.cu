@@ -615,18 +615,23 @@ __global__ void k_sample_lists(uint32_t lo, uint32_t nn, uint32_t stride, uint32
 // to the CTA tiers through F.defer_list.
 constexpr uint32_t kWLog = 9, kWSlots = 1u << kWLog, kWCap = 256, kWWarps = 8;
 
-__global__ void k_small_split(FusedJob F, uint32_t lo, uint32_t nn, uint32_t *lw, uint32_t *cw, uint32_t *lr,
-                              uint32_t *cr) {
+// Route by the bound b(n) = sum over I(n) of (|e| - 1) >= |N(n)|: b <= kWCap -> tier W, b <= the
+// A table's capacity -> tier A (it cannot overflow), larger -> straight to tier M (skipping a
+// traversal in A that would only overflow: on power-law inputs nearly every pin visit is a new
+// neighbour, so b is close to |N(n)|).
+__global__ void k_small_split(FusedJob F, uint32_t lo, uint32_t nn, uint32_t capA, uint32_t *lw, uint32_t *cw,
+                              uint32_t *lr, uint32_t *cr, uint32_t *lm, uint32_t *cm) {
   const ScoreJob &J = F.S;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
     const uint32_t n = lo + i;
     uint64_t b = 0;
-    for (uint64_t k = J.inc_off[n]; k < J.inc_off[n + 1] && b <= kWCap; ++k) {
+    for (uint64_t k = J.inc_off[n]; k < J.inc_off[n + 1] && b <= capA; ++k) {
       const uint32_t e = J.inc[k];
       b += J.edge_off[e + 1] - J.edge_off[e] - 1;
     }
     if (b <= kWCap) lw[atomicAdd(cw, 1u)] = n;
-    else lr[atomicAdd(cr, 1u)] = n;
+    else if (b <= capA) lr[atomicAdd(cr, 1u)] = n;
+    else lm[atomicAdd(cm, 1u)] = n;
   }
 }
 
@@ -847,7 +852,7 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
     uint32_t *cnt2 = scratch_zero<uint32_t>(c, 2, &st);
     if (st) return st;
     HGP_TRY(launch(c, "small_split", k_small_split, dim3(div_up(L.hn, 256) < 4096 ? div_up(L.hn, 256) : 4096), dim3(256),
-                   0, F, F.S.lo, L.hn, lw, cnt2, lr, cnt2 + 1));
+                   0, F, F.S.lo, L.hn, (1u << kFALog) / 2, lw, cnt2, lr, cnt2 + 1, L.la, L.ca));
     FusedJob FW = F;
     FW.list = lw; FW.list_count = cnt2; FW.defer_list = lr; FW.defer_count = cnt2 + 1;
     HGP_TRY(launch(c, "nbrscore_W", k_nbrscore_w<PIMAX>, dim3(16 * sm), dim3(kWWarps * 32), 0, FW));
