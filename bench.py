@@ -303,6 +303,8 @@ def main():
     ap.add_argument("--no-refine", action="store_true", help="skip the f1 quality / f3-f4 refinement-step leg")
     ap.add_argument("--no-hier", action="store_true", help="skip the whole-hierarchy leg (implies --no-refine)")
     ap.add_argument("--dominant", default=None, help="kernel name for the roofline (default: measured top kernel)")
+    ap.add_argument("--share-device", action="store_true",
+                    help="testing the N>1 code path on one GPU: every rank on cuda:0, gloo instead of NCCL")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -317,9 +319,14 @@ def main():
     from paper_2605_20497_b200 import hgp
 
     assert args.warmup >= 3 or os.environ.get("HGP_BENCH_ALLOW_SHORT"), "timing rules need >= 3 warm-up steps"
+    if args.share_device:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.share_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w, hg, omega, delta, pi, cap = _workload(args.workload, args.seed)
     N, E, P = hg.num_nodes, hg.num_edges, hg.num_pins
     stream = torch.cuda.current_stream()
@@ -352,7 +359,7 @@ def main():
             states = [shard.RankState(rank, bounds[rank], bounds[rank + 1])]
             cg, info = shard.level_sharded(ctx, g, params, states, comm, True, cand, match, gamma)
             cnb, nb = states[0].nb, None
-            vt = torch.tensor([info.V, cnb.V], dtype=torch.int64, device="cuda")
+            vt = torch.tensor([info.V, cnb.V], dtype=torch.int64, device="cpu" if args.share_device else "cuda")
             dist.all_reduce(vt)                                          # V and V' summed over the ranks
             st = {"Nc": cg.N, "Ec": cg.E, "Pc": cg.P, "Vc": int(vt[1].item()), "V": int(vt[0].item()),
                   "matched_per_round": [info.pairs],
@@ -369,7 +376,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if args.share_device else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -459,6 +466,21 @@ def main():
                 "level_ms": [round(l["ms"]["total"], 3) for l in levels],
                 "level_nodes": [l["N"] for l in levels],
                 "matched_fraction": [round(2 * sum(l["matched_per_round"]) / max(l["N"], 1), 4) for l in levels]}
+        # the same hierarchy with f2 (leftover pairing, HGP_FLAG_LEFTOVER): how close the stop
+        # rule's ceil(W / Omega) gets
+        pf2 = hgp.params(omega, delta, pi, noise_seed=args.seed, noise_cap=cap, flags=hgp.FLAG_LEFTOVER)
+        g2 = hgp.build_csr(ctx, N, dev["edge_off"], dev["edge_nsrc"], dev["pins"], dev["edge_w"], dev["node_w"])
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        _, cg2, cnb2, lv2 = hgp.coarsen(ctx, g2, pf2)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        Wt = int(hg.node_w.astype(np.int64).sum())
+        hier["with_f2"] = {"levels": len(lv2), "coarsest_nodes": cg2.N, "total_coarsening_ms": f0.elapsed_time(f1),
+                           "stop_target_ceil_W_over_omega": -(-Wt // omega) if omega < hgpgen.UNBOUNDED else 1}
+        hier["stop_target_ceil_W_over_omega"] = hier["with_f2"]["stop_target_ceil_W_over_omega"]
+        for x in (g2, cg2, cnb2):
+            x.free()
         if not args.no_refine:
             hier_q, refine = refine_leg(hgp, ctx, hierarchy, omega, delta, stream)
             hier["initial_partition"] = hier_q
@@ -466,9 +488,10 @@ def main():
         def hierarchy_sharded():
             g = hgp.build_csr(ctx, N, dev["edge_off"], dev["edge_nsrc"], dev["pins"], dev["edge_w"], dev["node_w"])
             rho, levels, cg, states = shard.coarsen_sharded(ctx, g, params, comm)
+            n_last = cg.N
             for x in [g, cg] + [s_.nb for s_ in states]:
                 x.free()
-            return levels, cg.N
+            return levels, n_last
         hierarchy_sharded()
         barrier()
         t_0 = time.perf_counter()
@@ -528,7 +551,9 @@ def main():
                    "delta": "inf" if delta == hgpgen.UNBOUNDED else delta, "pi": pi, "noise_cap": cap,
                    "seed": args.seed,
                    "parallelism": "1 GPU" if world == 1 else
-                   f"{world} node-range shards: a2+a3 sharded, cand + N(n) all-gathered (NCCL), a1/a4/a5 replicated",
+                   f"{world} ranks: a2+a3 on node ranges, a5 edges on edge ranges, a5 N' on coarse node ranges; "
+                   f"X1 cand all-gather, X2 pre-merge coarse-edge all-gather, X3 halo send/recv (NCCL); a1, a4 and "
+                   f"the merge replicated",
                    "l2": "inputs (%.0f MB) larger than L2" % (h2d_bytes / 1e6)},
         "gpu_launches": launches,
         "clocks": clk,

@@ -81,11 +81,25 @@ class DistComm:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.local = [self.rank]
+        # gloo moves host memory: device tensors are staged through the host (tests, --share-device)
+        self.stage = dist.get_backend(group) == "gloo"
+
+    def _out(self, t: torch.Tensor, like: torch.Tensor) -> torch.Tensor:
+        return t.to(like.device) if self.stage else t
 
     def allgather(self, xs: list[torch.Tensor]) -> list[torch.Tensor]:
-        return allgather_v(xs[0].contiguous(), self.group)
+        x = xs[0].contiguous()
+        outs = allgather_v(x.cpu() if self.stage else x, self.group)
+        return [self._out(o, x) for o in outs]
 
     def alltoall(self, send: list[list[torch.Tensor]]) -> list[list[torch.Tensor]]:
+        if self.stage:
+            dev = send[0][0].device
+            recv = DistComm._alltoall(self, [[x.cpu() for x in send[0]]])
+            return [[r.to(dev) for r in recv[0]]]
+        return DistComm._alltoall(self, send)
+
+    def _alltoall(self, send: list[list[torch.Tensor]]) -> list[list[torch.Tensor]]:
         mine = [x.contiguous() for x in send[0]]
         dev = mine[0].device
         sz = torch.tensor([x.numel() for x in mine], dtype=torch.int64, device=dev)

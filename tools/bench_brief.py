@@ -15,7 +15,8 @@ for path in sys.argv[1:]:
     print("  roofline", r.get("kernel"), "frac %.4f" % r.get("frac", 0), "ms/launch", r.get("ms_per_launch"))
     h = d.get("hierarchy")
     if h:
-        print("  hierarchy ms %.1f levels %d" % (h["total_coarsening_ms"], h["levels"]), h["level_ms"][:6])
+        print("  hierarchy ms %.1f levels %d" % (h["total_coarsening_ms"], h["levels"]), h.get("level_ms", [])[:6],
+              h.get("phase_ms_total", ""))
     if d.get("e2e"):
         print("  e2e %.3e" % d["e2e"]["value"])
     print("  clocks", d.get("clocks"))
