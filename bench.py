@@ -75,7 +75,7 @@ def algorithmic_bytes(step: str, N, E, P, V, pi, Nc=0, Ec=0, Pc=0, Vc=0) -> int:
     raise KeyError(step)
 
 
-KERNEL_STEP = {"nbrscore": "a2+a3", "pairs_total": "a2+a3", "fused_pack": "a2+a3", "validate": "a1", "check": "a1", "segsort": "a1", "inc_": "a1", "fill_mu": "a1", "max_deg": "a1",
+KERNEL_STEP = {"nbrscore": "a2+a3", "hub_": "a2+a3", "small_split": "a2+a3", "pairs_total": "a2+a3", "fused_pack": "a2+a3", "validate": "a1", "check": "a1", "segsort": "a1", "inc_": "a1", "fill_mu": "a1", "max_deg": "a1",
                "radix_": "a1", "edge_pairs": "a2", "nbrs_": "a2", "nbr_": "a2", "score_": "a3", "round_": "a4", "jump_": "a4",
                "fill_none": "a4"}
 

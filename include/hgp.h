@@ -165,7 +165,8 @@ HGP_API hgp_status hgp_sync(hgp_ctx *ctx);
  * level-0 kernel first runs tier A on every 64th node; default 65536), "fused_pool_cap" (capacity of
  * the fused kernel's first neighbour pool, 0 = automatic), "unfused" (1: every node takes the
  * unfused a2 -> a3 path), "inc_radix" (1: incidence transpose by radix sort), "debug_sync" (1:
- * synchronise and trace every launch on stderr). Unknown names and negative values: HGP_E_ARG. */
+ * synchronise and trace every launch on stderr), "no_hub" (1: hub nodes on the global-memory tiers
+ * instead of the key-partitioned hub tiers). Unknown names and negative values: HGP_E_ARG. */
 HGP_API hgp_status hgp_ctx_set_option(hgp_ctx *ctx, const char *name, int64_t value);
 /* Instrumentation: from hgp_profile_begin on, every kernel launch whose internal name contains
  * name_filter (e.g. "score_A") is bracketed by CUDA events on the ctx stream; hgp_profile_end
@@ -198,6 +199,9 @@ enum {
   HGP_TIER_CNBRS_C = 16,     /* a5 coarse neighbours, global-memory tables */
   HGP_TIER_JUMP = 17,        /* a4 pointer-jumping fallback (nodes of over-long best-child chains) */
   HGP_TIER_FUSED_W = 18,     /* fused a2+a3, one warp per small node (<= 256 pin visits) */
+  HGP_TIER_FUSED_H = 19,     /* fused a2+a3, hub nodes: key-partitioned shared tables (hub.cu) */
+  HGP_TIER_CNBRS_H = 20,     /* a5 coarse neighbours of hub coarse nodes, key-partitioned */
+  HGP_TIER_CNBRS_A2 = 21,    /* a5 coarse neighbours, 8192-slot table (between A and M) */
   HGP_TIERS = 24
 };
 /* HOST out[HGP_TIERS] <- the counters (synchronises); reset != 0 zeroes them afterwards. */

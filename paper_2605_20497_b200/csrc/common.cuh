@@ -66,6 +66,7 @@ struct hgp_ctx {
     bool unfused = false;                // every node on the unfused a2 -> a3 path (test hook)
     bool inc_radix = false;              // a1/a5 incidence transpose by radix sort (measured slower)
     bool debug_sync = false;             // serialise and trace every launch
+    bool no_hub = false;                 // hub nodes on the global-memory tiers (test hook)
   } opt;
   // profiling: CUDA events around every launch whose name contains prof_filter
   std::string prof_filter;
@@ -113,6 +114,19 @@ struct ApiScope {
 inline bool once_per_device(uint64_t *mask, int dev) {
   const unsigned long long bit = 1ull << (dev & 63);
   return (__atomic_fetch_or(reinterpret_cast<unsigned long long *>(mask), bit, __ATOMIC_ACQ_REL) & bit) == 0;
+}
+
+// CTAs of `kernel` that are resident at once on the whole GPU (occupancy x SMs): the grid of a
+// persistent grid-stride kernel. A larger grid leaves CTAs waiting for a whole resident CTA's
+// share of the list to finish (a second, partial wave: the makespan grows by up to 2x).
+template <class K>
+inline uint32_t resident_grid(const hgp_ctx *c, K kernel, int threads, size_t smem) {
+  int per = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem) != cudaSuccess || per < 1) {
+    cudaGetLastError();
+    per = 1;
+  }
+  return (uint32_t)per * (uint32_t)c->sm_count;
 }
 
 #define HGP_CUDA(x)                                                                              \

@@ -409,17 +409,29 @@ struct BoundIn {   // |N(a)| + |N(b)| per coarse node
   }
 };
 
-__global__ void k_cnbr_classify(const uint64_t *bound_off, uint32_t Nc, uint32_t capA, uint32_t capM, uint32_t capB,
-                                uint32_t *listM, uint32_t *listB, uint32_t *listC, uint32_t *counts,
-                                unsigned long long *maxb) {
+__global__ void k_cnbr_classify(const uint64_t *bound_off, uint32_t Nc, uint32_t capA, uint32_t capA2, uint32_t capM,
+                                uint32_t capB, uint32_t *listA2, uint32_t *listM, uint32_t *listB, uint32_t *listC,
+                                uint32_t *counts, unsigned long long *maxb) {
   uint64_t mx = 0;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < Nc; c += gridDim.x * blockDim.x) {
     const uint64_t d = bound_off[c + 1] - bound_off[c];
     if (d > capA) {
-      if (d <= capM) listM[atomicAdd(&counts[0], 1u)] = c;
+      if (d <= capA2) listA2[atomicAdd(&counts[3], 1u)] = c;
+      else if (d <= capM) listM[atomicAdd(&counts[0], 1u)] = c;
       else if (d <= capB) listB[atomicAdd(&counts[1], 1u)] = c;
       else { listC[atomicAdd(&counts[2], 1u)] = c; mx = d > mx ? d : mx; }
     }
+  }
+  mx = warp_max(mx);
+  if (lane_id() == 0 && mx) atomicMax(maxb, (unsigned long long)mx);
+}
+
+__global__ void k_list_max_bound(const uint64_t *bound_off, const uint32_t *list, const uint32_t *count,
+                                 unsigned long long *maxb) {
+  uint64_t mx = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < *count; i += gridDim.x * blockDim.x) {
+    const uint32_t c = list[i];
+    mx = max(mx, bound_off[c + 1] - bound_off[c]);
   }
   mx = warp_max(mx);
   if (lane_id() == 0 && mx) atomicMax(maxb, (unsigned long long)mx);
@@ -463,7 +475,218 @@ __global__ void k_count_kept(const uint32_t *rep, uint32_t E, uint32_t *out) {
   if (lane_id() == 0 && s) atomicAdd(out, s);
 }
 
+// ---- hub coarse nodes (|N(a)| + |N(b)| above tier B), key-partitioned like the fused hub tier
+// (hub.cu): the entries gamma(v) | flag are bucketed by a hash of gamma(v) into k(c) partitions
+// whose entry counts all fit half of an 8192-slot table (the size pass doubles k until they do,
+// so an item can never overflow: no fallback after N'(c) is partly written in place); one CTA
+// per partition deduplicates its bucket with OR-ed purge flags and appends its unflagged keys to
+// N'(c) (one atomic per partition on c's counter). Same set as tiers A-C (a union of per-key
+// decisions that do not depend on the partition).
+constexpr uint32_t kCHLog = 13, kCHCap = 1u << (kCHLog - 1), kCHMaxParts = 4096, kCHThreads = 256;
+
+__device__ __forceinline__ uint32_t chub_part(uint32_t m, uint32_t k) {   // independent of hash_slot
+  uint32_t h = m * 0x85EBCA77u;
+  h ^= h >> 15;
+  h *= 0xC2B2AE3Du;
+  h ^= h >> 13;
+  return __umulhi(h, k);
+}
+
+struct CHubJob {
+  CNbrJob J;
+  const uint32_t *list, *list_count;   // coarse nodes (relative ids)
+  uint32_t *hk;                        // [list] partitions (0: left to tier C)
+  uint64_t *hb;                        // [list] entries |N(a)| + |N(b)|
+  const uint64_t *item_off, *vis_off;  // [list] exclusive scans of hk / hb
+  uint32_t *ibase, *ilen, *inode;      // [items] bucket (relative to vis_off), length, list index
+  uint32_t *bkey;                      // [sum hb] gamma(v) | purge flag of v
+  uint32_t *hcnt;                      // [list] |N'(c)| so far
+  uint32_t *lu, *lu_count;             // -> tier C
+};
+
+// entries of c = {a, b}: N(a) then N(b)
+struct CEntries {
+  uint64_t a0, na, b0, n;
+  __device__ CEntries(const CNbrJob &J, uint32_t c) {
+    const uint32_t a = J.mem0[c], b = J.mem1[c];
+    uint64_t a1, b1 = 0;
+    b0 = 0;
+    if (J.nb_off) { a0 = J.nb_off[a]; a1 = J.nb_off[a + 1]; if (b != kNone) { b0 = J.nb_off[b]; b1 = J.nb_off[b + 1]; } }
+    else { a0 = J.nb_start[a]; a1 = a0 + J.nb_len[a]; if (b != kNone) { b0 = J.nb_start[b]; b1 = b0 + J.nb_len[b]; } }
+    na = a1 - a0;
+    n = na + (b1 - b0);
+  }
+  __device__ uint64_t at(uint64_t j) const { return j < na ? a0 + j : b0 + (j - na); }
+};
+
+// size (MODE 0): k(c) with every partition's entry count <= kCHCap; scatter (MODE 1): bucket
+// offsets, then the entries into their buckets. One CTA per listed coarse node.
+template <int MODE>
+__global__ void __launch_bounds__(kCHThreads) k_chub_visit(CHubJob H) {
+  constexpr uint32_t NW = kCHThreads / 32;
+  __shared__ uint32_t s_h[kCHMaxParts];
+  __shared__ uint32_t s_w[NW];
+  __shared__ uint32_t s_max;
+  const CNbrJob &J = H.J;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t total = *H.list_count;
+  uint64_t purged = 0;
+  for (uint32_t i = blockIdx.x; i < total; i += gridDim.x) {
+    const uint32_t c = H.list[i];
+    const CEntries X(J, c);
+    const uint32_t self = c + J.cbase;
+    uint32_t k = MODE == 0 ? (uint32_t)max((uint64_t)1, (X.n + kCHCap / 2 - 1) / (kCHCap / 2)) : H.hk[i];
+    if (k == 0 || k > kCHMaxParts) {                                // CTA-uniform: tier C takes it
+      if (MODE == 0 && tid == 0) { H.hk[i] = 0; H.hb[i] = 0; H.lu[atomicAdd(H.lu_count, 1u)] = c; }
+      continue;
+    }
+    while (true) {
+      for (uint32_t r = tid; r < k; r += kCHThreads) s_h[r] = 0;
+      if (tid == 0) s_max = 0;
+      __syncthreads();
+      for (uint64_t j = tid; j < X.n; j += kCHThreads) {
+        const uint32_t v = J.nbr[X.at(j)];
+        if (MODE == 1) purged += (v & kPurge) != 0;                 // (hubs only: tier C counts its own)
+        const uint32_t key = __ldg(J.gamma + (v & kIdMask));
+        if (key != self) atomicAdd(&s_h[chub_part(key, k)], 1u);
+      }
+      __syncthreads();
+      if (MODE == 1) break;
+      uint32_t mx = 0;
+      for (uint32_t r = tid; r < k; r += kCHThreads) mx = max(mx, s_h[r]);
+      mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+      if (lane == 0) atomicMax(&s_max, mx);
+      __syncthreads();
+      const uint32_t m = s_max;
+      __syncthreads();                                              // s_max / s_h rewritten next
+      if (m <= kCHCap || 2 * k > kCHMaxParts) {
+        if (tid == 0) {
+          const bool fits = m <= kCHCap;
+          H.hk[i] = fits ? k : 0;
+          H.hb[i] = fits ? X.n : 0;
+          H.hcnt[i] = 0;
+          if (!fits) H.lu[atomicAdd(H.lu_count, 1u)] = c;
+        }
+        break;
+      }
+      k *= 2;
+    }
+    if (MODE == 1) {
+      // bucket offsets: exclusive scan of the histogram; items; then the scatter with cursors
+      const uint64_t it0 = H.item_off[i], vo = H.vis_off[i];
+      const uint32_t per = (k + kCHThreads - 1) / kCHThreads, r0 = min(k, tid * per), r1 = min(k, r0 + per);
+      uint32_t run = 0;
+      for (uint32_t r = r0; r < r1; ++r) run += s_h[r];
+      const uint32_t wincl = warp_incl_scan(run);
+      if (lane == 31) s_w[w] = wincl;
+      __syncthreads();
+      uint32_t base = wincl - run;
+#pragma unroll
+      for (uint32_t q = 0; q < NW; ++q) base += q < w ? s_w[q] : 0u;
+      for (uint32_t r = r0; r < r1; ++r) {
+        const uint32_t cn = s_h[r];
+        H.ibase[it0 + r] = base;
+        H.ilen[it0 + r] = cn;
+        H.inode[it0 + r] = i;
+        s_h[r] = base;                                              // own entries only: no race
+        base += cn;
+      }
+      __syncthreads();
+      for (uint64_t j = tid; j < X.n; j += kCHThreads) {
+        const uint32_t v = J.nbr[X.at(j)];
+        const uint32_t key = __ldg(J.gamma + (v & kIdMask));
+        if (key == self) continue;
+        const uint32_t pos = atomicAdd(&s_h[chub_part(key, k)], 1u);
+        H.bkey[vo + pos] = key | (v & kPurge);
+      }
+      __syncthreads();                                              // s_h / s_w reused next node
+    }
+  }
+  if (MODE == 1) {
+    purged = warp_sum(purged);
+    if (lane == 0 && purged) atomicAdd(J.purged, (unsigned long long)purged);
+  }
+}
+
+// one CTA per partition: dedup with OR-ed flags, then the unflagged keys appended to N'(c)
+__global__ void __launch_bounds__(kCHThreads) k_chub_items(CHubJob H, uint32_t nitems) {
+  extern __shared__ __align__(16) uint32_t ckeys[];
+  constexpr uint32_t NW = kCHThreads / 32, S = 1u << kCHLog, hmask = S - 1;
+  __shared__ uint32_t s_w[NW];
+  __shared__ uint32_t s_pos;
+  const CNbrJob &J = H.J;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t keys_s = opaque_u32(smem_u32addr(ckeys));
+  for (uint32_t j = tid; j < S / 4; j += kCHThreads) reinterpret_cast<uint4 *>(ckeys)[j] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+  __syncthreads();
+  for (uint32_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const uint32_t i = H.inode[it];
+    const uint32_t c = H.list[i];
+    const uint64_t bb = H.vis_off[i] + H.ibase[it];
+    const uint32_t len = H.ilen[it];
+    for (uint32_t j = tid; j < len; j += kCHThreads) {
+      const uint32_t x = H.bkey[bb + j];
+      const uint32_t key = x & kIdMask, fl = x & kPurge;
+      uint32_t slot = hash_slot(key, kCHLog);
+      uint32_t kk = lds_u32(keys_s + 4 * slot);
+      while (true) {                                                // load <= 1/2: terminates
+        if (kk == kEmpty) {
+          kk = cas_u32(keys_s + 4 * slot, kEmpty, x);
+          if (kk == kEmpty) break;
+        }
+        if ((kk & kIdMask) == key) {
+          if (fl && !(kk & kPurge)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(keys_s + 4 * slot), "r"(kPurge) : "memory");
+          break;
+        }
+        slot = (slot + 1) & hmask;
+        kk = lds_u32(keys_s + 4 * slot);
+      }
+    }
+    __syncthreads();
+    // kept keys (unflagged; kEmpty has bit 31 set): count, one position claim, write + clear
+    constexpr uint32_t SW = S / NW;                                 // warp w owns [w SW, (w+1) SW)
+    uint32_t cnt = 0;
+    for (uint32_t j = w * SW + lane; j < (w + 1) * SW; j += 32) cnt += !(ckeys[j] & kPurge);
+    cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    if (lane == 0) s_w[w] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t t = 0;
+      for (uint32_t q = 0; q < NW; ++q) t += s_w[q];
+      s_pos = t ? atomicAdd(&H.hcnt[i], t) : 0u;
+    }
+    __syncthreads();
+    const CEntries X(J, c);
+    const uint64_t base = J.pool ? J.bound_off[c] : 0;
+    uint32_t wpos = s_pos;
+    for (uint32_t q = 0; q < w; ++q) wpos += s_w[q];
+    const uint32_t lt = (1u << lane) - 1;
+    for (uint32_t j0 = w * SW; j0 < (w + 1) * SW; j0 += 32) {
+      const uint32_t k = ckeys[j0 + lane];
+      const bool keep = !(k & kPurge);
+      const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+      if (keep) *cnbr_out(J, base, X.a0, X.na, X.b0, wpos + __popc(bal & lt)) = k;
+      wpos += __popc(bal);
+      if (k != kEmpty) ckeys[j0 + lane] = kEmpty;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_chub_finish(CHubJob H) {
+  const uint32_t total = *H.list_count;
+  uint32_t done = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    if (H.hk[i] == 0) continue;
+    H.J.cnt[H.list[i]] = H.hcnt[i];
+    ++done;
+  }
+  done = warp_sum(done);
+  if (lane_id() == 0 && done) tier_add(H.J.tiers, HGP_TIER_CNBRS_H, done);
+}
+
 static constexpr uint32_t kCALog = 12, kCAThreads = 256;   // 4096 slots: 16 KB, <= 2048 entries
+static constexpr uint32_t kCA2Log = 13;                     // 8192 slots: 32 KB, <= 4096 entries (5 CTAs/SM)
 static constexpr uint32_t kCMLog = 14, kCMThreads = 256;   // 16384 slots: 64 KB, <= 8192 entries (3 CTAs/SM)
 static constexpr uint32_t kCBLog = 15, kCBThreads = 256;   // 32768 slots: 128 KB, <= 16384 entries
 
@@ -648,7 +871,7 @@ static hgp_status cnbrs_impl(hgp_ctx *c, CNbrJob J, uint32_t clo, uint32_t chi, 
   // segments of its members (C5: saves V entries, ~40 GB)
   uint32_t *pool = inplace ? nullptr : scratch_raw<uint32_t>(c, Vb, &st);
   uint32_t *ccnt = scratch_raw<uint32_t>(c, Nc, &st);
-  uint32_t *lists = scratch_raw<uint32_t>(c, 3 * (size_t)Nc, &st);
+  uint32_t *lists = scratch_raw<uint32_t>(c, 4 * (size_t)Nc, &st);   // M, B, C, A2
   uint32_t *counts = scratch_zero<uint32_t>(c, 4, &st);
   unsigned long long *misc = scratch_zero<unsigned long long>(c, 2, &st);   // purged, max bound (tier C)
   unsigned int *maxes = scratch_zero<unsigned int>(c, 2, &st);
@@ -664,14 +887,20 @@ static hgp_status cnbrs_impl(hgp_ctx *c, CNbrJob J, uint32_t clo, uint32_t chi, 
   J.pool = pool; J.cnt = ccnt; J.Nc = Nc; J.purged = misc; J.tiers = c->d_tiers; J.tier = HGP_TIER_CNBRS_A;
   J.nbr_w = inplace ? const_cast<uint32_t *>(J.nbr) : nullptr;
   J.cbase = clo;
-  const uint32_t capA = 1u << (kCALog - 1), capM = 1u << (kCMLog - 1), capB = 1u << (kCBLog - 1);
+  const uint32_t capA = 1u << (kCALog - 1), capA2 = 1u << (kCA2Log - 1), capM = 1u << (kCMLog - 1), capB = 1u << (kCBLog - 1);
   J.list = nullptr; J.list_count = nullptr; J.cap = capA; J.log2s = kCALog;
   const uint32_t gA = Nc < 64u * c->sm_count ? (Nc ? Nc : 1) : 64u * c->sm_count;
   if (Nc) HGP_TRY(launch(c, "coarse_nbrs_A", k_coarse_nbrs<kCAThreads, true>, dim3(gA), dim3(kCAThreads), 5u << kCALog, J));
   if (Nc) HGP_TRY(launch(c, "cnbr_classify", k_cnbr_classify, dim3(grid_n(c, Nc)), dim3(256), 0, (const uint64_t *)bound_off,
-                         Nc, capA, capM, capB, lists, lists + Nc, lists + 2 * (size_t)Nc, counts, misc + 1));
-  uint32_t hc[3];
-  HGP_TRY(read_back(c, counts, 12, hc));
+                         Nc, capA, capA2, capM, capB, lists + 3 * (size_t)Nc, lists, lists + Nc, lists + 2 * (size_t)Nc,
+                         counts, misc + 1));
+  uint32_t hc[4];
+  HGP_TRY(read_back(c, counts, 16, hc));
+  if (hc[3]) {   // between A and M: 40 KB, 5 CTAs/SM (M's 80 KB tables allow 2)
+    J.list = lists + 3 * (size_t)Nc; J.list_count = counts + 3; J.cap = capA2; J.log2s = kCA2Log; J.tier = HGP_TIER_CNBRS_A2;
+    const uint32_t g2 = resident_grid(c, k_coarse_nbrs<kCMThreads, true>, kCMThreads, 5u << kCA2Log);
+    HGP_TRY(launch(c, "coarse_nbrs_A2", k_coarse_nbrs<kCMThreads, true>, dim3(g2), dim3(kCMThreads), 5u << kCA2Log, J));
+  }
   if (hc[0]) {
     J.list = lists; J.list_count = counts; J.cap = capM; J.log2s = kCMLog; J.tier = HGP_TIER_CNBRS_M;
     HGP_TRY(launch(c, "coarse_nbrs_M", k_coarse_nbrs<kCMThreads, true>, dim3(2 * c->sm_count), dim3(kCMThreads),
@@ -682,15 +911,57 @@ static hgp_status cnbrs_impl(hgp_ctx *c, CNbrJob J, uint32_t clo, uint32_t chi, 
     HGP_TRY(launch(c, "coarse_nbrs_B", k_coarse_nbrs<kCBThreads, true>, dim3(c->sm_count), dim3(kCBThreads),
                    5u << kCBLog, J));
   }
+  uint32_t *listC = lists + 2 * (size_t)Nc, *countC = counts + 2;
+  if (hc[2] && !c->opt.no_hub) {   // hubs: key-partitioned shared tables; what they leave -> tier C
+    const uint32_t hn = hc[2];
+    CHubJob H{};
+    H.J = J;
+    H.list = listC; H.list_count = countC;
+    H.hk = scratch_raw<uint32_t>(c, hn, &st);
+    H.hb = scratch_raw<uint64_t>(c, hn, &st);
+    H.hcnt = scratch_raw<uint32_t>(c, hn, &st);
+    uint64_t *item_off = scratch_raw<uint64_t>(c, (size_t)hn + 1, &st);
+    uint64_t *vis_off = scratch_raw<uint64_t>(c, (size_t)hn + 1, &st);
+    H.lu = scratch_raw<uint32_t>(c, hn, &st);
+    H.lu_count = scratch_zero<uint32_t>(c, 1, &st);
+    if (st) return st;
+    H.item_off = item_off; H.vis_off = vis_off;
+    const uint32_t gh = hn < 4u * c->sm_count ? hn : 4u * c->sm_count;
+    HGP_TRY(launch(c, "chub_size", k_chub_visit<0>, dim3(gh), dim3(kCHThreads), 0, H));
+    uint64_t nitems = 0, nvis = 0;
+    HGP_TRY(scan_exclusive(c, InU32{H.hk}, hn, item_off, &nitems));
+    HGP_TRY(scan_exclusive(c, InU64{H.hb}, hn, vis_off, &nvis));
+    if (nitems > 0xFFFFFFFFull) return set_error(HGP_E_OVERFLOW, "coarse hub tier: too many partitions");
+    if (nitems) {
+      H.ibase = scratch_raw<uint32_t>(c, nitems, &st);
+      H.ilen = scratch_raw<uint32_t>(c, nitems, &st);
+      H.inode = scratch_raw<uint32_t>(c, nitems, &st);
+      H.bkey = scratch_raw<uint32_t>(c, nvis, &st);
+      if (st) return st;
+      HGP_TRY(launch(c, "chub_scatter", k_chub_visit<1>, dim3(gh), dim3(kCHThreads), 0, H));
+      const size_t smem = 4u << kCHLog;
+      const uint32_t gi0 = resident_grid(c, k_chub_items, kCHThreads, smem);
+      HGP_TRY(launch(c, "chub_items", k_chub_items, dim3(nitems < gi0 ? (uint32_t)nitems : gi0), dim3(kCHThreads), smem, H,
+                     (uint32_t)nitems));
+      HGP_TRY(launch(c, "chub_finish", k_chub_finish, dim3(grid_n(c, hn)), dim3(256), 0, H));
+    }
+    HGP_TRY(read_back(c, H.lu_count, 4, &hc[2]));
+    listC = H.lu; countC = H.lu_count;
+  }
   if (hc[2]) {
     uint64_t mb = 0;
+    if (listC != lists + 2 * (size_t)Nc) {   // the hub tier's leftovers: their own max bound
+      HGP_CUDA(cudaMemsetAsync(misc + 1, 0, 8, c->stream));
+      HGP_TRY(launch(c, "cnbr_maxb", k_list_max_bound, dim3(grid_n(c, hc[2])), dim3(256), 0, (const uint64_t *)bound_off,
+                     (const uint32_t *)listC, (const uint32_t *)countC, misc + 1));
+    }
     HGP_TRY(read_u64(c, (const uint64_t *)(misc + 1), &mb));
     uint32_t lg = kCBLog;
     while ((1ull << (lg - 1)) < mb) ++lg;
     const uint32_t ctas = hc[2] < (uint32_t)c->sm_count ? hc[2] : (uint32_t)c->sm_count;
     uint32_t *gtab = scratch_raw<uint32_t>(c, (size_t)ctas << lg, &st);
     if (st) return st;
-    J.list = lists + 2 * (size_t)Nc; J.list_count = counts + 2; J.cap = 0xFFFFFFFFu; J.log2s = lg; J.gtab = gtab;
+    J.list = listC; J.list_count = countC; J.cap = 0xFFFFFFFFu; J.log2s = lg; J.gtab = gtab;
     J.tier = HGP_TIER_CNBRS_C;
     HGP_TRY(launch(c, "coarse_nbrs_C", k_coarse_nbrs<256, false>, dim3(ctas), dim3(256), 0, J));
   }

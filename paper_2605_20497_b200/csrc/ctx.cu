@@ -277,6 +277,7 @@ hgp_status hgp_ctx_set_option(hgp_ctx *c, const char *name, int64_t value) {
   else if (k == "unfused") c->opt.unfused = value != 0;
   else if (k == "inc_radix") c->opt.inc_radix = value != 0;
   else if (k == "debug_sync") c->opt.debug_sync = value != 0;
+  else if (k == "no_hub") c->opt.no_hub = value != 0;
   else return set_error(HGP_E_ARG, "hgp_ctx_set_option: unknown option '%s'", name);
   return HGP_OK;
 }

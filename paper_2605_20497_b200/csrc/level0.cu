@@ -17,177 +17,16 @@
 #include "hashset.cuh"
 #include "scan.cuh"
 #include "score_common.cuh"
+#include "fused.cuh"
 
 namespace hgp {
-
-constexpr uint32_t kProbeCap = 64;   // longer probe runs mean the table is (nearly) full
-
-struct FusedJob {
-  ScoreJob S;                     // level arrays + parameters + cand
-  const uint32_t *list, *list_count;   // nodes to process (nullptr: all of [lo, hi))
-  uint32_t log2s;                 // table size
-  uint32_t *pool;
-  uint64_t pool_cap;
-  unsigned long long *pool_cursor;
-  uint64_t *start;                // [hi-lo] pool offset of each node's N(n)
-  uint32_t *cnt;                  // [hi-lo]
-  uint32_t *defer_list, *defer_count;     // table too small / wide -> next tier
-  uint32_t *pool_list, *pool_count;       // pool full (cnt[n] holds the exact count) -> second pool
-  uint64_t start_bias;                    // added to every start written
-  const uint64_t *cv;                     // [E] c(e), Eq.5 term in 2^-24 fixed point
-  const uint2 *wmu;                       // [N] (size, in_mu) packed for the validity test
-  unsigned long long *tiers;              // work counters (hgp_tier_counts)
-  int tier;
-};
-
-// The validity test of Eq.6 on one (key, acc) pair of the dense list; writes the
-// N(n) entry (purge flag on invalid neighbours) and returns the shared-edge count and
-// the neighbour. Every sum fits 32 bits: sizes sum to < 2^32 (reading #2), |in(n) ∪ in(m)| <= E.
-struct EvalCtx {
-  uint32_t wn, inn, imask, om32, de32, ib;
-};
-__device__ __forceinline__ EvalCtx eval_ctx(const ScoreJob &J, uint32_t n, uint32_t ib) {
-  EvalCtx e;
-  e.wn = J.node_w[n];
-  e.inn = J.in_mu[n];
-  e.ib = ib;
-  e.imask = ib ? (uint32_t)((1ull << ib) - 1) : 0u;
-  e.om32 = J.omega >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)J.omega;
-  e.de32 = J.delta >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)J.delta;   // HGP_UNBOUNDED too
-  return e;
-}
-__device__ __forceinline__ bool eval_one(const FusedJob &F, const EvalCtx &E, uint2 d, uint64_t pos, uint32_t &cnt) {
-  const uint32_t v = d.x, x = d.y;
-  cnt = E.ib < 32 ? x >> E.ib : 0u;
-  const uint32_t inter = x & E.imask;
-  const uint2 wm = __ldg(F.wmu + v);                               // (size(m), in_mu(m)): one gather
-  // |in(n) ∪ in(m)| = in_mu(n) + in_mu(m) - inter; inter <= in_mu(m)
-  const bool ok = E.wn + wm.x <= E.om32 && E.inn + (wm.y - inter) <= E.de32;
-  F.pool[pos] = ok ? v : (v | kPurge);
-  return ok;
-}
-
-// Phase 3 of k_nbrscore, PACKED: every score of the node is < 2^32 (S1 + cap < 2^32), so
-// (score << 32 | id) is one u64 key ordering (score desc, id desc) exactly (Eq.6's max_id).
-// Each warp takes chunks of 4 entries per lane; per chunk, pi rounds of a warp argmax (two 32-bit
-// REDUX: the score word, then the id among its holders) over the chunk's keys and the warp's
-// running list (carried by lanes 0..pi-1) rebuild that list. Warp 0 then merges the NW lists.
-template <int PIMAX, int THREADS>
-__device__ __forceinline__ void eval_packed(const ScoreJob &J, const FusedJob &F, uint32_t n, uint32_t count,
-                                            const uint2 *dense, uint32_t g32, uint32_t ib, uint64_t base,
-                                            uint64_t *s_tops) {
-  constexpr uint32_t NW = THREADS / 32;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const EvalCtx E = eval_ctx(J, n, ib);
-  const uint32_t cap32 = (uint32_t)J.noise_cap;
-  uint64_t carry = 0;                                              // lane r < pi: the warp's r-th best
-  for (uint32_t c0 = w * 32; c0 < count; c0 += 4 * THREADS) {     // warp-uniform
-    uint64_t k[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t i = c0 + u * THREADS + lane;
-      k[u] = 0;
-      if (i < count) {
-        const uint2 d = dense[i];
-        uint32_t cnt;
-        if (eval_one(F, E, d, base + i, cnt)) {
-          uint32_t s32 = cnt * g32;                                // eta(n, m) < 2^32
-          if (cap32) {
-            const uint64_t key = ((uint64_t)min(n, d.x) << 32) | max(n, d.x);
-            s32 += (uint32_t)__umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);   // uniform in [0, cap]
-          }
-          k[u] = ((uint64_t)s32 << 32) | d.x;
-        }
-      }
-    }
-    uint64_t nc = 0;
-    for (uint32_t r = 0; r < J.pi; ++r) {
-      uint64_t lm = carry;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) lm = k[u] > lm ? k[u] : lm;
-      const uint32_t hi = (uint32_t)(lm >> 32);
-      const uint32_t mhi = __reduce_max_sync(0xFFFFFFFFu, hi);
-      if (mhi == 0) break;                                         // every score >= 1: nothing left
-      const uint32_t mlo = __reduce_max_sync(0xFFFFFFFFu, hi == mhi ? (uint32_t)lm : 0u);
-      const uint64_t K = ((uint64_t)mhi << 32) | mlo;              // ids are distinct: one holder
-      if (carry == K) carry = 0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (k[u] == K) k[u] = 0;
-      if (lane == r) nc = K;
-    }
-    carry = nc;
-  }
-  if (lane < J.pi) s_tops[w * PIMAX + lane] = carry;
-  __syncthreads();
-  if (w == 0) {
-    TopK<PIMAX> t2;
-#pragma unroll
-    for (int i = 0; i < PIMAX; ++i) t2.k[i] = 0;
-    for (uint32_t i = lane; i < NW * J.pi; i += 32) topk_insert<PIMAX>(t2, J.pi, s_tops[(i / J.pi) * PIMAX + i % J.pi]);
-    warp_topk_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX);
-    __syncwarp();
-    for (uint32_t r = lane; r < J.pi; r += 32) {
-      const uint64_t kk = s_tops[NW * PIMAX + r];
-      hgp_cand cd;
-      cd.score = kk >> 32;
-      cd.id = kk ? (uint32_t)kk : kNone;
-      cd.pad = 0;
-      J.cand[(uint64_t)n * J.pi + r] = cd;
-    }
-  }
-}
-
-// Phase 3, general: scores up to 2^62 as (u64 score, id) lists per thread, merged per warp and
-// by warp 0.
-template <int PIMAX, int THREADS>
-__device__ __forceinline__ void eval_top(const ScoreJob &J, const FusedJob &F, uint32_t n, uint32_t count,
-                                         const uint2 *dense, uint64_t g, uint32_t ib, uint64_t base, uint64_t *s_tops,
-                                         uint32_t *s_topi) {
-  constexpr uint32_t NW = THREADS / 32;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const EvalCtx E = eval_ctx(J, n, ib);
-  Top<PIMAX> top;
-#pragma unroll
-  for (int i = 0; i < PIMAX; ++i) { top.s[i] = 0; top.id[i] = 0; }
-  for (uint32_t i = tid; i < count; i += THREADS) {
-    const uint2 d = dense[i];
-    uint32_t cnt;
-    if (!eval_one(F, E, d, base + i, cnt)) continue;
-    uint64_t sc = (uint64_t)cnt * g;
-    if (J.noise_cap) {
-      const uint64_t key = ((uint64_t)min(n, d.x) << 32) | max(n, d.x);
-      sc += __umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);
-    }
-    top_insert<PIMAX>(top, J.pi, sc, d.x);
-  }
-  warp_top_merge<PIMAX>(top, J.pi, s_tops + w * PIMAX, s_topi + w * PIMAX);
-  __syncthreads();
-  if (w == 0) {
-    Top<PIMAX> t2;
-#pragma unroll
-    for (int i = 0; i < PIMAX; ++i) { t2.s[i] = 0; t2.id[i] = 0; }
-    for (uint32_t i = lane; i < NW * J.pi; i += 32) {
-      const uint32_t ww = i / J.pi, r = i % J.pi;
-      top_insert<PIMAX>(t2, J.pi, s_tops[ww * PIMAX + r], s_topi[ww * PIMAX + r]);
-    }
-    warp_top_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX, s_topi + NW * PIMAX);
-    __syncwarp();
-    for (uint32_t r = lane; r < J.pi; r += 32) {
-      hgp_cand cd;
-      cd.score = s_tops[NW * PIMAX + r];
-      cd.id = cd.score ? s_topi[NW * PIMAX + r] : kNone;
-      cd.pad = 0;
-      J.cand[(uint64_t)n * J.pi + r] = cd;
-    }
-  }
-}
 
 // Shared-memory layout of k_nbrscore: keys[S] | acc[S] | dense (key, acc) pairs uint2[S/2] | rows
 // of the current tile of incident edges: uint4 {flat end, pins index - flat start (mod 2^32),
 // flat start of dst(e), add of a src pin} and u32 {add of a dst pin}.
 constexpr uint32_t kKT = 128;     // incident edges per tile
 constexpr uint32_t fused_smem(uint32_t lg) { return (12u << lg) + kKT * 20u; }
+constexpr uint32_t fused_smem_list(uint32_t lg) { return (9u << lg) + kKT * 20u; }   // keys, acc, u16 list
 
 // predicated shared CAS: lanes with p == false return `dflt` without touching memory
 __device__ __forceinline__ uint32_t cas_u32_if(bool p, uint32_t a, uint32_t cmp, uint32_t val, uint32_t dflt) {
@@ -197,12 +36,6 @@ __device__ __forceinline__ uint32_t cas_u32_if(bool p, uint32_t a, uint32_t cmp,
                : "r"(a), "r"(cmp), "r"(val), "r"((uint32_t)p)
                : "memory");
   return old;
-}
-
-__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-  return v;
 }
 
 // One CTA per node n (grid-stride over the node list): the fused a2 + a3 traversal of I(n).
@@ -221,7 +54,12 @@ __device__ __forceinline__ uint4 lds_v4(uint32_t a) {
 //  phase 2   validity, purge flags, noise and top-Pi over the dense slot list; N(n) to the pool.
 //  reset     only the slots used (the table is cleared once per CTA).
 // Requires P < 2^32 (32-bit pin indices; the caller routes larger levels to the unfused path).
-template <int THREADS, int PIMAX, int MINB, int LOG2S>
+// LIST (power-law inputs, routed by b(n)): every newly claimed slot is appended to a slot list
+// (one warp-aggregated shared atomic per window with claims), so phase 2 reads and clears just the
+// node's slots — no sweeps over the S-slot table and no dense array (M's table then fits 3 CTAs
+// per SM). Worth it when most visits are first visits (V ~ T); the sweep form is kept for the
+// SNN-like inputs where a key is visited ~10 times and claims are rare.
+template <int THREADS, int PIMAX, int MINB, int LOG2S, bool LIST = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
   extern __shared__ __align__(16) unsigned char dyn[];
   constexpr uint32_t NW = THREADS / 32;
@@ -230,31 +68,39 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
   __shared__ uint32_t s_topi[(NW + 1) * PIMAX];
   __shared__ uint64_t s_sum[NW], s_g[NW];
   __shared__ uint32_t s_wsum[NW];
-  __shared__ uint32_t s_full, s_defer;
+  __shared__ uint32_t s_full, s_defer, s_n;
   __shared__ unsigned long long s_start;
   const ScoreJob &J = F.S;
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   constexpr uint32_t S = 1u << LOG2S, ucap = S / 2, hmask = S - 1;
   uint32_t *keys = reinterpret_cast<uint32_t *>(dyn);
   uint32_t *acc = keys + S;
-  uint2 *dense = reinterpret_cast<uint2 *>(acc + S);
-  uint4 *rows = reinterpret_cast<uint4 *>(dense + S / 2);
+  uint2 *dense = reinterpret_cast<uint2 *>(acc + S);               // (sweep form)
+  uint16_t *slist = reinterpret_cast<uint16_t *>(acc + S);         // (LIST: ucap slots)
+  static_assert(!LIST || S <= 65536, "u16 slot list");
+  uint4 *rows = LIST ? reinterpret_cast<uint4 *>(slist + S / 2) : reinterpret_cast<uint4 *>(dense + S / 2);
   uint32_t *rowd = reinterpret_cast<uint32_t *>(rows + kKT);
   // shared-window addresses kept in registers (no rematerialisation inside the pin loop)
   const uint32_t keys_s = opaque_u32(smem_u32addr(keys)), acc_s = keys_s + 4 * S;
   const uint32_t rows_s = opaque_u32(smem_u32addr(rows)), rowd_s = rows_s + 16 * kKT;
   const uint32_t total = F.list_count ? *F.list_count : J.hi - J.lo;
+  const bool unb = J.delta == HGP_UNBOUNDED;
+  const uint64_t mxin = J.max_in_mu ? *J.max_in_mu : 0xFFFFFFFFull;   // max in_mu of the level
   for (uint32_t i = tid; i < S / 4; i += THREADS) {
     reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     reinterpret_cast<uint4 *>(acc)[i] = make_uint4(0, 0, 0, 0);
   }
-  if (tid == 0) s_full = 0;
+  if (tid == 0) { s_full = 0; s_n = 0; }
   uint32_t done = 0;
   for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
     const uint32_t n = F.list ? F.list[t] : J.lo + t;
     const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1], iin = i0 + J.inc_nin[n];
     const uint64_t deg = i1 - i0;
     const uint32_t inn = J.in_mu[n];
+    // Eq.6's inbound test cannot fail for n when even the level's largest in_mu keeps it true
+    // (in_mu(n) + max in_mu <= Delta): then inter(n, m) is never needed — ib = 0, no mu terms,
+    // and with a uniform c(e) every pin visit adds exactly 1 (the ADD1 pin loop)
+    const bool noint = unb || (uint64_t)inn + mxin <= J.delta;
     // ---- prologue: the first tile's edge data stays in registers
     const bool mine = tid < kKT && i0 + tid < i1;
     uint32_t tlen = 0, tns = 0, tmu = 0;
@@ -265,12 +111,19 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       tlen = (uint32_t)(J.edge_off[te + 1] - ta);
       tns = J.edge_nsrc[te];
       tce = F.cv[te];
-      tmu = i0 + tid < iin ? J.edge_mu[te] : 0u;
+      tmu = !noint && i0 + tid < iin ? J.edge_mu[te] : 0u;
     }
     const uint64_t c0 = deg ? F.cv[J.inc[i0]] : 0;                 // broadcast load
     bool diff = mine && tce != c0;
+    uint64_t sum = tce;                                            // S1 = sum of c(e), published with B1
 #pragma unroll 1
-    for (uint64_t k = i0 + kKT + tid; k < i1; k += THREADS) diff |= F.cv[J.inc[k]] != c0;
+    for (uint64_t k = i0 + kKT + tid; k < i1; k += THREADS) {
+      const uint64_t ce = F.cv[J.inc[k]];
+      diff |= ce != c0;
+      sum += ce;
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) s_sum[w] = sum;
     // tile-0 scan of |e|; does every row of the tile have >= 32 pins (then a lane's next flat
     // position, 32 further on, is at most one row end away)?
     // (bit 31 of a warp's published sum: one of its rows is short; sums stay < 2^29 + 2^24)
@@ -284,35 +137,39 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       g = c0 ? c0 : 1;
       S1g = deg;
       small = (unsigned __int128)c0 * deg + J.noise_cap < ((unsigned __int128)1 << 32);
-    } else {   // rare on SNN inputs: mixed edge sizes or weights
-      uint64_t sum = tce, gg = tce;
-#pragma unroll 1
-      for (uint64_t k = i0 + kKT + tid; k < i1; k += THREADS) {
-        const uint64_t ce = F.cv[J.inc[k]];
-        sum += ce;
-        gg = gcd64(gg, ce);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-        const uint64_t og = __shfl_xor_sync(0xFFFFFFFFu, gg, o);
-        if (og != gg) gg = gcd64(gg, og);
-      }
-      if (lane == 0) { s_sum[w] = sum; s_g[w] = gg; }
-      __syncthreads();
+    } else {   // mixed edge sizes or weights (power-law inputs: most nodes)
+      // S1 (published with B1); the gcd (a binary-GCD reduction: thousands of instructions per
+      // node, measured to dominate small power-law nodes) only when g = 1 leaves the packed form
+      // inexact
       uint64_t S1 = 0;
-      g = 0;
 #pragma unroll
-      for (uint32_t q = 0; q < NW; ++q) {
-        S1 += s_sum[q];
-        const uint64_t x = s_g[q];
-        if (x != g) g = gcd64(g, x);
+      for (uint32_t q = 0; q < NW; ++q) S1 += s_sum[q];
+      const uint32_t ib0 = inn && !noint ? 32 - __clz(inn) : 0;
+      g = 1;
+      if ((((unsigned __int128)(S1 + 1)) << ib0) > ((unsigned __int128)1 << 32)) {
+        uint64_t gg = tce;
+#pragma unroll 1
+        for (uint64_t k = i0 + kKT + tid; k < i1; k += THREADS) gg = gcd64(gg, F.cv[J.inc[k]]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint64_t og = __shfl_xor_sync(0xFFFFFFFFu, gg, o);
+          if (og != gg) gg = gcd64(gg, og);
+        }
+        if (lane == 0) s_g[w] = gg;
+        __syncthreads();
+        g = 0;
+#pragma unroll
+        for (uint32_t q = 0; q < NW; ++q) {
+          const uint64_t x = s_g[q];
+          if (x != g) g = gcd64(g, x);
+        }
+        if (g == 0) g = 1;
       }
-      if (g == 0) g = 1;
-      S1g = S1 / g;
+      S1g = g == 1 ? S1 : S1 / g;
       small = (unsigned __int128)S1 + J.noise_cap < ((unsigned __int128)1 << 32);
     }
-    const uint32_t ib = inn ? 32 - __clz(inn) : 0;
+    const uint32_t ib = inn && !noint ? 32 - __clz(inn) : 0;
+    const bool add1 = noint && !nonuni;                            // every visit adds 1
     if ((((unsigned __int128)(S1g + 1)) << ib) > ((unsigned __int128)1 << 32)) {   // packed form inexact
       if (tid == 0) F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
       continue;                                                    // nothing was inserted
@@ -332,7 +189,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
           len = (uint32_t)(J.edge_off[e + 1] - a);
           ns = J.edge_nsrc[e];
           ce = F.cv[e];
-          mu = t0 + tid < iin ? J.edge_mu[e] : 0u;
+          mu = !noint && t0 + tid < iin ? J.edge_mu[e] : 0u;
         }
         incl = warp_incl_scan(len);
         const bool sh = __any_sync(0xFFFFFFFFu, tid < kt && len < 32);
@@ -349,7 +206,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       const bool longrows = anyshort == 0;
       if (tid < kt) {
         const uint32_t ex = woff + incl - len;
-        const uint32_t as = (uint32_t)((nonuni && ce != g ? ce / g : 1ull) << ib);
+        const uint32_t as = (uint32_t)((!nonuni || ce == g ? 1ull : g == 1 ? ce : ce / g) << ib);
         rows[tid] = make_uint4(ex + len, (uint32_t)a - ex, ex + ns, as);
         rowd[tid] = as + mu;                                       // m in dst(e), e in in(n)
       }
@@ -360,7 +217,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       // keys (rare) probe on.
       auto insert4 = [&](const uint32_t (&m)[4], const uint32_t (&add)[4], const bool (&val)[4], auto full_tag) {
         constexpr bool FULL = decltype(full_tag)::value;
-        uint32_t sl[4], kk[4], miss = 0;
+        uint32_t sl[4], kk[4], miss = 0, clm = 0;                  // clm (LIST): slots claimed, per u
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           sl[u] = hash_slot(m[u], LOG2S);
@@ -370,8 +227,44 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
         for (int u = 0; u < 4; ++u) {
           // claim an empty home (CAS; a first visit); hit if the home now holds m; add the packed
           // term — a miss adds 0 to the slot it looked at (no branch); else report a miss
-          uint32_t ms;
-          if (FULL) {
+          uint32_t ms, cl = 0;
+          if (LIST && FULL) {
+            asm volatile(
+                "{\n .reg .pred pc, ph, pk;\n .reg .b32 o;\n"
+                " setp.eq.u32 pc, %3, -1;\n"
+                " mov.b32 o, %3;\n"
+                " @pc atom.shared.cas.b32 o, [%2], -1, %4;\n"
+                " setp.eq.u32 pk, o, -1;\n"                          // o == -1 only if the CAS claimed
+                " setp.eq.u32 ph, o, %4;\n"
+                " or.pred ph, ph, pk;\n"
+                " selp.u32 o, %5, 0, ph;\n"
+                " red.shared.add.u32 [%2+%6], o;\n"
+                " selp.u32 %0, 0, 1, ph;\n"
+                " selp.u32 %1, 1, 0, pk;\n}"
+                : "=r"(ms), "=r"(cl)
+                : "r"(keys_s + 4 * sl[u]), "r"(kk[u]), "r"(m[u]), "r"(add[u]), "n"(4 * S)
+                : "memory");
+          } else if (LIST) {
+            asm volatile(
+                "{\n .reg .pred pv, pc, ph, pk;\n .reg .b32 o;\n"
+                " setp.ne.u32 pv, %3, 0;\n"
+                " setp.eq.and.u32 pc, %4, -1, pv;\n"
+                " mov.b32 o, %4;\n"
+                " @pc atom.shared.cas.b32 o, [%2], -1, %5;\n"
+                " setp.eq.and.u32 pk, o, -1, pv;\n"
+                " setp.eq.u32 ph, o, %5;\n"
+                " or.pred ph, ph, pk;\n"
+                " and.pred ph, ph, pv;\n"
+                " selp.u32 o, %6, 0, ph;\n"
+                " red.shared.add.u32 [%2+%7], o;\n"
+                " not.pred ph, ph;\n"
+                " and.pred ph, ph, pv;\n"
+                " selp.u32 %0, 1, 0, ph;\n"
+                " selp.u32 %1, 1, 0, pk;\n}"
+                : "=r"(ms), "=r"(cl)
+                : "r"(keys_s + 4 * sl[u]), "r"((uint32_t)val[u]), "r"(kk[u]), "r"(m[u]), "r"(add[u]), "n"(4 * S)
+                : "memory");
+          } else if (FULL) {
             asm volatile(
                 "{\n .reg .pred pc, ph;\n .reg .b32 o;\n"
                 " setp.eq.u32 pc, %2, -1;\n"
@@ -405,6 +298,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
                 : "memory");
           }
           miss |= ms << u;
+          clm |= cl << u;
         }
         if (__any_sync(0xFFFFFFFFu, miss != 0)) {                  // collision-displaced keys: probe on
 #pragma unroll
@@ -419,11 +313,30 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
               k2 = lds_u32(keys_s + 4 * slot);
               if (k2 == kEmpty) {
                 k2 = cas_u32(keys_s + 4 * slot, kEmpty, m[u]);
-                if (k2 == kEmpty) break;
+                if (k2 == kEmpty) {
+                  if (LIST) { clm |= 1u << u; sl[u] = slot; }         // claimed further on
+                  break;
+                }
               }
             } while (k2 != m[u]);
             if (ok) red_add_u32(acc_s + 4 * slot, add[u]);
             else full = true;
+          }
+        }
+        if (LIST && __any_sync(0xFFFFFFFFu, clm != 0)) {            // append the claimed slots
+          const uint32_t c = __popc(clm);
+          const uint32_t incl = warp_incl_scan(c);
+          uint32_t base = 0;
+          if (lane == 31 && incl) base = atomicAdd(&s_n, incl);    // lane 31's inclusive sum: the warp's
+          base = __shfl_sync(0xFFFFFFFFu, base, 31);
+          uint32_t p = base + incl - c;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if ((clm >> u) & 1u) {
+              if (p < ucap) slist[p] = (uint16_t)sl[u];
+              else full = true;                                  // more keys than the tier holds
+              ++p;
+            }
           }
         }
       };
@@ -442,8 +355,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       uint4 ra = lds_v4(rows_s + 16 * k);
       uint32_t rd = lds_u32(rowd_s + 4 * k);
       // one 128-pin window of this warp's flat range; FULL: the window lies inside [flo, fhi)
-      auto window = [&](uint32_t f0, auto full_tag, auto long_tag) {
+      // ADD1: every visit adds 1 (noint, uniform c(e)): only (row end, pins base) are tracked
+      auto window = [&](uint32_t f0, auto full_tag, auto long_tag, auto add1_tag) {
         constexpr bool FULL = decltype(full_tag)::value, LONG = decltype(long_tag)::value;
+        constexpr bool ADD1 = decltype(add1_tag)::value;
         uint32_t m[4], add[4];
         bool val[4];
 #pragma unroll
@@ -455,102 +370,169 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
             // predicated single-row advance replaces the loop (no branch); the first position
             // of the warp's range was placed by the binary search
             const uint32_t lim = FULL ? 0xFFFFFFFFu : fhi;
-            asm volatile(
-                "{\n .reg .pred pa;\n .reg .b32 ad;\n"
-                " setp.ge.u32 pa, %7, %0;\n"
-                " setp.lt.and.u32 pa, %7, %9, pa;\n"
-                " @pa add.u32 %4, %4, 1;\n"
-                " @pa mad.lo.u32 ad, %4, 16, %6;\n"
-                " @pa ld.shared.v4.u32 {%0, %1, %2, %3}, [ad];\n"
-                " @pa mad.lo.u32 ad, %4, 4, %8;\n"
-                " @pa ld.shared.u32 %5, [ad];\n}"
-                : "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w), "+r"(k), "+r"(rd)
-                : "r"(rows_s), "r"(f), "r"(rowd_s), "r"(lim)
-                : "memory");
+            if (ADD1) {
+              asm volatile(
+                  "{\n .reg .pred pa;\n .reg .b32 ad;\n"
+                  " setp.ge.u32 pa, %3, %0;\n"
+                  " setp.lt.and.u32 pa, %3, %4, pa;\n"
+                  " @pa add.u32 %2, %2, 1;\n"
+                  " @pa mad.lo.u32 ad, %2, 16, %5;\n"
+                  " @pa ld.shared.v2.u32 {%0, %1}, [ad];\n}"
+                  : "+r"(ra.x), "+r"(ra.y), "+r"(k)
+                  : "r"(f), "r"(lim), "r"(rows_s)
+                  : "memory");
+            } else {
+              asm volatile(
+                  "{\n .reg .pred pa;\n .reg .b32 ad;\n"
+                  " setp.ge.u32 pa, %7, %0;\n"
+                  " setp.lt.and.u32 pa, %7, %9, pa;\n"
+                  " @pa add.u32 %4, %4, 1;\n"
+                  " @pa mad.lo.u32 ad, %4, 16, %6;\n"
+                  " @pa ld.shared.v4.u32 {%0, %1, %2, %3}, [ad];\n"
+                  " @pa mad.lo.u32 ad, %4, 4, %8;\n"
+                  " @pa ld.shared.u32 %5, [ad];\n}"
+                  : "+r"(ra.x), "+r"(ra.y), "+r"(ra.z), "+r"(ra.w), "+r"(k), "+r"(rd)
+                  : "r"(rows_s), "r"(f), "r"(rowd_s), "r"(lim)
+                  : "memory");
+            }
           } else if (val[u]) {
-            while (f >= ra.x) { ++k; ra = lds_v4(rows_s + 16 * k); rd = lds_u32(rowd_s + 4 * k); }   // next edge(s)
+            while (f >= ra.x) {                                    // next edge(s)
+              ++k;
+              if (ADD1) {
+                const uint2 r2 = lds_v2(rows_s + 16 * k);
+                ra.x = r2.x; ra.y = r2.y;
+              } else {
+                ra = lds_v4(rows_s + 16 * k);
+                rd = lds_u32(rowd_s + 4 * k);
+              }
+            }
           }
           m[u] = val[u] ? __ldg(J.pins + (ra.y + f)) : 0u;
-          add[u] = f >= ra.z ? rd : ra.w;
+          add[u] = ADD1 ? 1u : (f >= ra.z ? rd : ra.w);
         }
         insert4(m, add, val, full_tag);
       };
       uint32_t f0 = flo;
-      if (longrows) {
-        for (; f0 + 128 <= fhi; f0 += 128) window(f0, std::true_type{}, std::true_type{});
-        if (f0 < fhi) window(f0, std::false_type{}, std::true_type{});
-      } else {
-        for (; f0 + 128 <= fhi; f0 += 128) window(f0, std::true_type{}, std::false_type{});
-        if (f0 < fhi) window(f0, std::false_type{}, std::false_type{});
-      }
+      auto run = [&](auto add1_tag) {
+        if (longrows) {
+          for (; f0 + 128 <= fhi; f0 += 128) window(f0, std::true_type{}, std::true_type{}, add1_tag);
+          if (f0 < fhi) window(f0, std::false_type{}, std::true_type{}, add1_tag);
+        } else {
+          for (; f0 + 128 <= fhi; f0 += 128) window(f0, std::true_type{}, std::false_type{}, add1_tag);
+          if (f0 < fhi) window(f0, std::false_type{}, std::false_type{}, add1_tag);
+        }
+      };
+      if (add1) run(std::true_type{});
+      else run(std::false_type{});
       if (full) s_full = 1;
       __syncthreads();                                             // B3: rows are rewritten next
       if (s_full) break;
     }
     if (deg == 0) __syncthreads();                                 // no tile barrier orders n's own key
-    // ---- phase 2a: count the occupied slots but n's own; warp w owns the slots [w S/NW, (w+1) S/NW),
-    //      read 4 per lane (LDS.128)
-    constexpr uint32_t SW = S / NW;
-    static_assert(SW % 128 == 0, "4 slots per lane per sweep step");
-    const uint32_t wbase = w * SW;
-    uint32_t c1 = 0;
-#pragma unroll 2
-    for (uint32_t j = 4 * lane; j < SW; j += 128) {
-      const uint4 k4 = lds_v4(keys_s + 4 * (wbase + j));
-      c1 += (uint32_t)(k4.x != kEmpty && k4.x != n) + (uint32_t)(k4.y != kEmpty && k4.y != n) +
-            (uint32_t)(k4.z != kEmpty && k4.z != n) + (uint32_t)(k4.w != kEmpty && k4.w != n);
-    }
-    const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c1);
-    if (lane == 0) s_wsum[w] = wc;
-    __syncthreads();                                               // B3'
-    uint32_t woff = 0, count = 0;
-#pragma unroll
-    for (uint32_t q = 0; q < NW; ++q) { const uint32_t x = s_wsum[q]; woff += q < w ? x : 0u; count += x; }
-    const bool over = s_full || count > ucap;                      // table too small: next tier
-    // ---- phase 2b: pool space for N(n) (thread 0); the warps move the occupied (key, acc) pairs
-    //      to the dense array and clear the table behind them (it is clean for the next node)
-    if (tid == 0) {
-      s_defer = 0;
-      if (over) {
-        F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
-      } else {
-        const unsigned long long st = atomicAdd(F.pool_cursor, (unsigned long long)count);
-        s_start = st;
-        F.cnt[n - J.lo] = count;
-        if (st + count > F.pool_cap) {
-          s_defer = 1;
-          F.pool_list[atomicAdd(F.pool_count, 1u)] = n;
+    if constexpr (LIST) {
+      // ---- phase 2 (LIST): the node's keys are the listed slots (n's own home is not listed)
+      const uint32_t count = s_n;
+      const bool over = s_full != 0;                               // probe cap or list overflow
+      if (tid == 0) {
+        keys[hash_slot(n, LOG2S)] = kEmpty;                          // n's home (self-visits added there)
+        acc[hash_slot(n, LOG2S)] = 0;
+        s_defer = 0;
+        if (over) {
+          F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
         } else {
-          F.start[n - J.lo] = st + F.start_bias;
+          const unsigned long long st = atomicAdd(F.pool_cursor, (unsigned long long)count);
+          s_start = st;
+          F.cnt[n - J.lo] = count;
+          if (st + count > F.pool_cap) {
+            s_defer = 1;
+            F.pool_list[atomicAdd(F.pool_count, 1u)] = n;
+          } else {
+            F.start[n - J.lo] = st + F.start_bias;
+          }
         }
       }
-    }
-#pragma unroll 2
-    for (uint32_t j = 4 * lane; j < SW; j += 128) {
-      const uint32_t ak = keys_s + 4 * (wbase + j);
-      const uint4 k4 = lds_v4(ak);
-      const uint4 a4 = lds_v4(ak + 4 * S);
-      const bool o0 = k4.x != kEmpty && k4.x != n, o1 = k4.y != kEmpty && k4.y != n;
-      const bool o2 = k4.z != kEmpty && k4.z != n, o3 = k4.w != kEmpty && k4.w != n;
-      const uint32_t c = (uint32_t)o0 + o1 + o2 + o3;
-      const uint32_t incl = warp_incl_scan(c);
-      if (!over) {
-        uint32_t p = woff + incl - c;
-        if (o0) dense[p++] = make_uint2(k4.x, a4.x);
-        if (o1) dense[p++] = make_uint2(k4.y, a4.y);
-        if (o2) dense[p++] = make_uint2(k4.z, a4.z);
-        if (o3) dense[p] = make_uint2(k4.w, a4.w);
+      __syncthreads();                                             // B4: s_start / s_defer; s_n read
+      if (tid == 0) { s_full = 0; s_n = 0; }
+      if (over) {                                                  // the list may be incomplete: sweep
+        for (uint32_t i = tid; i < S / 4; i += THREADS) {
+          reinterpret_cast<uint4 *>(keys)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+          reinterpret_cast<uint4 *>(acc)[i] = make_uint4(0, 0, 0, 0);
+        }
+        continue;                                                  // (next node's B1 orders the clear)
       }
-      woff += __shfl_sync(0xFFFFFFFFu, incl, 31);
-      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(ak), "r"(kEmpty) : "memory");
-      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(ak + 4 * S), "r"(0u) : "memory");
+      if (s_defer) {
+        for (uint32_t i = tid; i < count; i += THREADS) { const uint32_t sl = slist[i]; keys[sl] = kEmpty; acc[sl] = 0; }
+        continue;
+      }
+      if (tid == 0) ++done;
+      const ListSrc src{slist, keys_s, acc_s};                     // reads and clears each listed slot
+      if (small) eval_packed<PIMAX, THREADS>(J, F, n, count, src, (uint32_t)g, ib, s_start, s_tops, J.cand + (uint64_t)n * J.pi);
+      else eval_top<PIMAX, THREADS>(J, F, n, count, src, g, ib, s_start, s_tops, s_topi, J.cand + (uint64_t)n * J.pi);
+    } else {
+      // ---- phase 2a: count the occupied slots but n's own; warp w owns the slots [w S/NW, (w+1) S/NW),
+      //      read 4 per lane (LDS.128)
+      constexpr uint32_t SW = S / NW;
+      static_assert(SW % 128 == 0, "4 slots per lane per sweep step");
+      const uint32_t wbase = w * SW;
+      uint32_t c1 = 0;
+  #pragma unroll 2
+      for (uint32_t j = 4 * lane; j < SW; j += 128) {
+        const uint4 k4 = lds_v4(keys_s + 4 * (wbase + j));
+        c1 += (uint32_t)(k4.x != kEmpty && k4.x != n) + (uint32_t)(k4.y != kEmpty && k4.y != n) +
+              (uint32_t)(k4.z != kEmpty && k4.z != n) + (uint32_t)(k4.w != kEmpty && k4.w != n);
+      }
+      const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, c1);
+      if (lane == 0) s_wsum[w] = wc;
+      __syncthreads();                                               // B3'
+      uint32_t woff = 0, count = 0;
+  #pragma unroll
+      for (uint32_t q = 0; q < NW; ++q) { const uint32_t x = s_wsum[q]; woff += q < w ? x : 0u; count += x; }
+      const bool over = s_full || count > ucap;                      // table too small: next tier
+      // ---- phase 2b: pool space for N(n) (thread 0); the warps move the occupied (key, acc) pairs
+      //      to the dense array and clear the table behind them (it is clean for the next node)
+      if (tid == 0) {
+        s_defer = 0;
+        if (over) {
+          F.defer_list[atomicAdd(F.defer_count, 1u)] = n;
+        } else {
+          const unsigned long long st = atomicAdd(F.pool_cursor, (unsigned long long)count);
+          s_start = st;
+          F.cnt[n - J.lo] = count;
+          if (st + count > F.pool_cap) {
+            s_defer = 1;
+            F.pool_list[atomicAdd(F.pool_count, 1u)] = n;
+          } else {
+            F.start[n - J.lo] = st + F.start_bias;
+          }
+        }
+      }
+  #pragma unroll 2
+      for (uint32_t j = 4 * lane; j < SW; j += 128) {
+        const uint32_t ak = keys_s + 4 * (wbase + j);
+        const uint4 k4 = lds_v4(ak);
+        const uint4 a4 = lds_v4(ak + 4 * S);
+        const bool o0 = k4.x != kEmpty && k4.x != n, o1 = k4.y != kEmpty && k4.y != n;
+        const bool o2 = k4.z != kEmpty && k4.z != n, o3 = k4.w != kEmpty && k4.w != n;
+        const uint32_t c = (uint32_t)o0 + o1 + o2 + o3;
+        const uint32_t incl = warp_incl_scan(c);
+        if (!over) {
+          uint32_t p = woff + incl - c;
+          if (o0) dense[p++] = make_uint2(k4.x, a4.x);
+          if (o1) dense[p++] = make_uint2(k4.y, a4.y);
+          if (o2) dense[p++] = make_uint2(k4.z, a4.z);
+          if (o3) dense[p] = make_uint2(k4.w, a4.w);
+        }
+        woff += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(ak), "r"(kEmpty) : "memory");
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(ak + 4 * S), "r"(0u) : "memory");
+      }
+      __syncthreads();                                               // B4
+      if (tid == 0) s_full = 0;
+      if (over || s_defer) continue;                                 // (the table is already clean)
+      if (tid == 0) ++done;
+      if (small) eval_packed<PIMAX, THREADS>(J, F, n, count, DenseSrc{dense}, (uint32_t)g, ib, s_start, s_tops, J.cand + (uint64_t)n * J.pi);
+      else eval_top<PIMAX, THREADS>(J, F, n, count, DenseSrc{dense}, g, ib, s_start, s_tops, s_topi, J.cand + (uint64_t)n * J.pi);
     }
-    __syncthreads();                                               // B4
-    if (tid == 0) s_full = 0;
-    if (over || s_defer) continue;                                 // (the table is already clean)
-    if (tid == 0) ++done;
-    if (small) eval_packed<PIMAX, THREADS>(J, F, n, count, dense, (uint32_t)g, ib, s_start, s_tops);
-    else eval_top<PIMAX, THREADS>(J, F, n, count, dense, g, ib, s_start, s_tops, s_topi);
   }
   if (tid == 0) tier_add(F.tiers, F.tier, done);
 }
@@ -570,9 +552,15 @@ __global__ void k_fused_pack(const uint32_t *pool, const uint64_t *start, const 
   if (lane == 0) atomicMax(maxdeg, mx);
 }
 
-__global__ void k_pack_wmu(const uint32_t *node_w, const uint32_t *in_mu, uint32_t N, uint2 *wmu) {
-  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x)
+__global__ void k_pack_wmu(const uint32_t *node_w, const uint32_t *in_mu, uint32_t N, uint2 *wmu,
+                           unsigned int *max_in_mu) {
+  uint32_t mx = 0;
+  for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
     wmu[n] = make_uint2(node_w[n], in_mu[n]);
+    mx = max(mx, in_mu[n]);
+  }
+  mx = warp_max(mx);
+  if (lane_id() == 0 && mx) atomicMax(max_in_mu, mx);
 }
 
 __global__ void k_edge_cv(const uint64_t *edge_off, const uint32_t *edge_w, uint32_t E, uint32_t norm, uint64_t *cv) {
@@ -616,22 +604,24 @@ __global__ void k_sample_lists(uint32_t lo, uint32_t nn, uint32_t stride, uint32
 constexpr uint32_t kWLog = 9, kWSlots = 1u << kWLog, kWCap = 256, kWWarps = 8;
 
 // Route by the bound b(n) = sum over I(n) of (|e| - 1) >= |N(n)|: b <= kWCap -> tier W, b <= the
-// A table's capacity -> tier A (it cannot overflow), larger -> straight to tier M (skipping a
+// A table's capacity -> tier A (it cannot overflow), <= B's -> straight to tier M (skipping a
 // traversal in A that would only overflow: on power-law inputs nearly every pin visit is a new
-// neighbour, so b is close to |N(n)|).
-__global__ void k_small_split(FusedJob F, uint32_t lo, uint32_t nn, uint32_t capA, uint32_t *lw, uint32_t *cw,
-                              uint32_t *lr, uint32_t *cr, uint32_t *lm, uint32_t *cm) {
+// neighbour, so b is close to |N(n)|), larger -> the hub tier (hub.cu).
+__global__ void k_small_split(FusedJob F, uint32_t lo, uint32_t nn, uint32_t capA, uint32_t capB, uint32_t *lw,
+                              uint32_t *cw, uint32_t *lr, uint32_t *cr, uint32_t *lm, uint32_t *cm, uint32_t *lh,
+                              uint32_t *ch) {
   const ScoreJob &J = F.S;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += gridDim.x * blockDim.x) {
     const uint32_t n = lo + i;
     uint64_t b = 0;
-    for (uint64_t k = J.inc_off[n]; k < J.inc_off[n + 1] && b <= capA; ++k) {
+    for (uint64_t k = J.inc_off[n]; k < J.inc_off[n + 1] && b <= capB; ++k) {
       const uint32_t e = J.inc[k];
       b += J.edge_off[e + 1] - J.edge_off[e] - 1;
     }
     if (b <= kWCap) lw[atomicAdd(cw, 1u)] = n;
     else if (b <= capA) lr[atomicAdd(cr, 1u)] = n;
-    else lm[atomicAdd(cm, 1u)] = n;
+    else if (b <= capB) lm[atomicAdd(cm, 1u)] = n;
+    else lh[atomicAdd(ch, 1u)] = n;                                  // hub: straight to the hub tier
   }
 }
 
@@ -652,21 +642,23 @@ __global__ void __launch_bounds__(kWWarps * 32) k_nbrscore_w(FusedJob F) {
     const uint32_t n = F.list[t];
     const uint64_t i0 = J.inc_off[n], i1 = J.inc_off[n + 1], iin = i0 + J.inc_nin[n];
     const uint32_t inn = J.in_mu[n];
-    // sum and gcd of c(e) over I(n): is the packed accumulator (eta/g << ib | inter) exact?
-    uint64_t sum = 0, gg = 0;
-    for (uint64_t k = i0 + lane; k < i1; k += 32) {
-      const uint64_t ce = F.cv[J.inc[k]];
-      sum += ce;
-      gg = gcd64(gg, ce);
-    }
+    // sum of c(e) over I(n); the gcd g only if g = 1 leaves the packed accumulator
+    // (eta/g << ib | inter) inexact (a binary-GCD reduction costs thousands of instructions)
+    uint64_t sum = 0;
+    for (uint64_t k = i0 + lane; k < i1; k += 32) sum += F.cv[J.inc[k]];
     sum = warp_sum(sum);
+    const uint32_t ib = inn ? 32 - __clz(inn) : 0;
+    uint64_t gg = 1;
+    if ((((unsigned __int128)(sum + 1)) << ib) > ((unsigned __int128)1 << 32)) {
+      gg = 0;
+      for (uint64_t k = i0 + lane; k < i1; k += 32) gg = gcd64(gg, F.cv[J.inc[k]]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t og = __shfl_xor_sync(0xFFFFFFFFu, gg, o);
-      if (og != gg) gg = gcd64(gg, og);
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t og = __shfl_xor_sync(0xFFFFFFFFu, gg, o);
+        if (og != gg) gg = gcd64(gg, og);
+      }
     }
     const uint64_t g = gg ? gg : 1;
-    const uint32_t ib = inn ? 32 - __clz(inn) : 0;
     const bool exact = (((unsigned __int128)(sum / g + 1)) << ib) <= ((unsigned __int128)1 << 32);
     const bool small = (unsigned __int128)sum + J.noise_cap < ((unsigned __int128)1 << 32);
     if (!exact || !small) {
@@ -687,7 +679,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_nbrscore_w(FusedJob F) {
         len = (uint32_t)(J.edge_off[e + 1] - ea);
         ns = J.edge_nsrc[e];
         const uint64_t ce = F.cv[e];
-        as = (uint32_t)((ce == g ? 1ull : ce / g) << ib);
+        as = (uint32_t)((ce == g ? 1ull : g == 1 ? ce : ce / g) << ib);
         ad = as + (c0 + lane < iin ? J.edge_mu[e] : 0u);           // m in dst(e), e in in(n)
       }
       const uint32_t incl = warp_incl_scan(len);
@@ -827,6 +819,7 @@ struct TierLists {
   uint32_t *la, *ca, *lm, *cm;          // A -> M, M -> B hand-off
   uint32_t *ld, *cd;                    // B -> unfused (appended)
   bool small_first;                     // route small nodes to tier W first (range input only)
+  bool list_mode = false;               // A and M in their LIST form (the routed power-law path)
 };
 
 
@@ -839,11 +832,18 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
                          fused_smem(kFMLog));
     cudaFuncSetAttribute(k_nbrscore<kFBThreads, PIMAX, 1, kFBLog>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          fused_smem(kFBLog));
+    cudaFuncSetAttribute(k_nbrscore<TA, PIMAX, MINB, kFALog, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         fused_smem_list(kFALog));
+    cudaFuncSetAttribute(k_nbrscore<kFMThreads, PIMAX, 3, kFMLog, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         fused_smem_list(kFMLog));
   }
   const uint32_t sm = c->sm_count;
   const uint32_t per_sm = MINB;                                     // exactly the resident CTAs
   const uint32_t gA = L.hn < per_sm * sm ? L.hn : per_sm * sm;
   if (gA == 0) return HGP_OK;
+  // M and B: exactly the resident CTAs (M's 98 KB table fits 2 per SM, not its register bound 3)
+  const uint32_t gM = resident_grid(c, k_nbrscore<kFMThreads, PIMAX, 3, kFMLog>, kFMThreads, fused_smem(kFMLog));
+  const uint32_t gB = resident_grid(c, k_nbrscore<kFBThreads, PIMAX, 1, kFBLog>, kFBThreads, fused_smem(kFBLog));
   if (!L.in_list && L.small_first) {
     // tier W first: nodes with <= kWCap pin visits, one warp each; the rest (and W's deferrals)
     // continue below as a list
@@ -852,12 +852,13 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
     uint32_t *cnt2 = scratch_zero<uint32_t>(c, 2, &st);
     if (st) return st;
     HGP_TRY(launch(c, "small_split", k_small_split, dim3(div_up(L.hn, 256) < 4096 ? div_up(L.hn, 256) : 4096), dim3(256),
-                   0, F, F.S.lo, L.hn, (1u << kFALog) / 2, lw, cnt2, lr, cnt2 + 1, L.la, L.ca));
+                   0, F, F.S.lo, L.hn, (1u << kFALog) / 2, (1u << kFBLog) / 2, lw, cnt2, lr, cnt2 + 1, L.la, L.ca,
+                   L.ld, L.cd));
     FusedJob FW = F;
     FW.list = lw; FW.list_count = cnt2; FW.defer_list = lr; FW.defer_count = cnt2 + 1;
     HGP_TRY(launch(c, "nbrscore_W", k_nbrscore_w<PIMAX>, dim3(16 * sm), dim3(kWWarps * 32), 0, FW));
     TierLists L2 = L;
-    L2.in_list = lr; L2.in_count = cnt2 + 1; L2.small_first = false;
+    L2.in_list = lr; L2.in_count = cnt2 + 1; L2.small_first = false; L2.list_mode = true;
     return fused_tiers_t<PIMAX, TA, MINB>(c, F, L2);
   }
   constexpr uint32_t kStride = 64;
@@ -883,7 +884,7 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
     F.tier = HGP_TIER_FUSED_A;
     if (4 * deferred > ns) {                                        // > 25 %: start in M
       F.log2s = kFMLog; F.tier = HGP_TIER_FUSED_M; F.defer_list = L.lm; F.defer_count = L.cm;
-      HGP_TRY(launch(c, "nbrscore_M", k_nbrscore<kFMThreads, PIMAX, 3, kFMLog>, dim3(3 * sm), dim3(kFMThreads),
+      HGP_TRY(launch(c, "nbrscore_M", k_nbrscore<kFMThreads, PIMAX, 3, kFMLog>, dim3(gM), dim3(kFMThreads),
                      fused_smem(kFMLog), F));
     } else {
       HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
@@ -891,14 +892,24 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
   } else {
     F.list = L.in_list; F.list_count = L.in_count; F.log2s = kFALog; F.tier = HGP_TIER_FUSED_A;
     F.defer_list = L.la; F.defer_count = L.ca;
-    HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
+    if (L.list_mode)
+      HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog, true>, dim3(gA), dim3(TA),
+                     fused_smem_list(kFALog), F));
+    else
+      HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
   }
   F.list = L.la; F.list_count = L.ca; F.log2s = kFMLog; F.tier = HGP_TIER_FUSED_M;
   F.defer_list = L.lm; F.defer_count = L.cm;
-  HGP_TRY(launch(c, "nbrscore_M", k_nbrscore<kFMThreads, PIMAX, 3, kFMLog>, dim3(3 * sm), dim3(kFMThreads), fused_smem(kFMLog), F));
+  if (L.list_mode) {   // 74.5 KB: 3 CTAs per SM (the sweep form's 98.5 KB allows 2)
+    const uint32_t gML = resident_grid(c, k_nbrscore<kFMThreads, PIMAX, 3, kFMLog, true>, kFMThreads, fused_smem_list(kFMLog));
+    HGP_TRY(launch(c, "nbrscore_M", k_nbrscore<kFMThreads, PIMAX, 3, kFMLog, true>, dim3(gML), dim3(kFMThreads),
+                   fused_smem_list(kFMLog), F));
+  } else {
+    HGP_TRY(launch(c, "nbrscore_M", k_nbrscore<kFMThreads, PIMAX, 3, kFMLog>, dim3(gM), dim3(kFMThreads), fused_smem(kFMLog), F));
+  }
   F.list = L.lm; F.list_count = L.cm; F.log2s = kFBLog; F.tier = HGP_TIER_FUSED_B;
   F.defer_list = L.ld; F.defer_count = L.cd;
-  HGP_TRY(launch(c, "nbrscore_B", k_nbrscore<kFBThreads, PIMAX, 1, kFBLog>, dim3(sm), dim3(kFBThreads), fused_smem(kFBLog), F));
+  HGP_TRY(launch(c, "nbrscore_B", k_nbrscore<kFBThreads, PIMAX, 1, kFBLog>, dim3(gB), dim3(kFBThreads), fused_smem(kFBLog), F));
   return HGP_OK;
 }
 
@@ -949,10 +960,13 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
                  dim3(256), 0, (const uint64_t *)g->edge_off, g->E, misc));
   uint64_t T = 0;
   HGP_TRY(read_u64(c, (const uint64_t *)misc, &T));
-  // pool estimate: min(T, 24 P) scaled to the range; nodes that do not fit get a second, exact pool
+  // pool: T = sum_n b(n) bounds V exactly (|N(n)| <= b(n) = sum over I(n) of (|e| - 1)), scaled to
+  // the range. A smaller estimate (24 P was used) sends every node past it through a second, exact
+  // pool — a second full traversal: on power-law inputs V ~ T (C3: V = 7.2e9 = 0.95 T, 24 P = 1.2e9)
+  // and the level paid both (measured: A+M+B 192 ms then 307 ms again).
   const double frac = g->N ? (double)nn / g->N : 1.0;
-  uint64_t pool_cap = (uint64_t)((T < 24 * g->P ? T : 24 * g->P) * (frac < 1.0 ? 1.25 * frac : 1.0)) + nn;
-  // at most 2^34 entries (64 GB; C5's 24 P would be 96 GB); nodes that do not fit go to the exact
+  uint64_t pool_cap = (uint64_t)(T * (frac < 1.0 ? 1.25 * frac : 1.0)) + nn;
+  // at most 2^34 entries (64 GB; C5's T would be 396 GB); nodes that do not fit go to the exact
   // second pool. (A cap from cudaMemGetInfo was measured to misfire: the caching allocator's
   // reserved blocks read as used, the pool shrank and the level took the slow second-pool path.)
   if (pool_cap > (1ull << 34)) pool_cap = 1ull << 34;
@@ -964,6 +978,7 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   uint32_t *pool = scratch_raw<uint32_t>(c, pool_cap, &st);
   if (st) return st;
   uint32_t *LA = lists, *LM = lists + nn, *LD = lists + 2 * (size_t)nn, *LP = lists + 3 * (size_t)nn;
+  // (counts 8: the nodes the hub tier leaves to the unfused path, listed in LA)
   // counts: 0 A->M, 1 M->B, 2 deferred (unfused), 3 pool overflow, 4/5 second pass A->M / M->B,
   // 6 second-pass pool overflow (impossible: exact pool), 7 max degree
   uint64_t *cv = scratch_raw<uint64_t>(c, g->E ? g->E : 1, &st);
@@ -971,9 +986,11 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   HGP_TRY(launch(c, "edge_cv", k_edge_cv, dim3(g->E ? (div_up(g->E, 256) < 4096 ? div_up(g->E, 256) : 4096) : 0), dim3(256), 0,
                  (const uint64_t *)g->edge_off, (const uint32_t *)g->edge_w, g->E, p->norm, cv));
   uint2 *wmu = scratch_raw<uint2>(c, g->N ? g->N : 1, &st);
+  unsigned int *mxin = scratch_zero<unsigned int>(c, 1, &st);
   if (st) return st;
   HGP_TRY(launch(c, "pack_wmu", k_pack_wmu, dim3(g->N ? (div_up(g->N, 256) < 4096 ? div_up(g->N, 256) : 4096) : 0),
-                 dim3(256), 0, (const uint32_t *)g->node_w, (const uint32_t *)g->in_mu, g->N, wmu));
+                 dim3(256), 0, (const uint32_t *)g->node_w, (const uint32_t *)g->in_mu, g->N, wmu, mxin));
+  J.max_in_mu = mxin;
   FusedJob F{};
   F.S = J;
   F.cv = cv;
@@ -1005,6 +1022,12 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
     else HGP_TRY(fused_tiers<16>(c, F2, L2));
     HGP_TRY(read_back(c, counts, sizeof(hc), hc));
     if (hc[6]) return set_error(HGP_E_INTERNAL, "fused a2+a3: exact second pool overflowed");
+  }
+  if (hc[2] && !all_unfused && !c->opt.no_hub) {   // hubs: key-partitioned shared tables (hub.cu); what they leave -> LA
+    HGP_TRY(hub_tier(c, F, LD, counts + 2, hc[2], LA, counts + 8));
+    HGP_TRY(read_back(c, counts + 8, 4, &hc[2]));
+    LD = LA;
+    HGP_CUDA(cudaMemcpyAsync(counts + 2, counts + 8, 4, cudaMemcpyDeviceToDevice, c->stream));
   }
   if (hc[2]) {   // unfused a2 + a3 for the nodes no fused tier could take (same results)
     uint32_t md = 0;

@@ -277,7 +277,7 @@ hgp_status nbrs_for_list(hgp_ctx *c, const hgp_csr *g, uint32_t lo, const uint32
     gtab = scratch_raw<uint32_t>(c, (size_t)c->sm_count << lg, &st);
     if (st) return st;
   }
-  uint64_t pool_cap = hb[0] < 8 * g->P + hcount ? hb[0] : 8 * g->P + hcount;
+  uint64_t pool_cap = hb[0] + hcount < (1ull << 34) ? hb[0] + hcount : (1ull << 34);   // the exact bound
   for (int attempt = 0;; ++attempt) {
     if (pool_cap == 0) pool_cap = 1;
     uint32_t *pool = scratch_raw<uint32_t>(c, pool_cap, &st);
@@ -332,7 +332,7 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
     out->nbr = dalloc_n<uint32_t>(c, 1, &st);
     return st;
   }
-  // pool capacity: min(T, 24 P + nn) with T = sum_e |e|(|e|-1) >= total pre-dedup candidates
+  // pool capacity: T = sum_e |e|(|e|-1) >= total pre-dedup candidates
   unsigned long long *misc = scratch_zero<unsigned long long>(c, 4, &st);   // T, cursor, bound, -
   uint32_t *counters = scratch_zero<uint32_t>(c, 8, &st);                  // ovf1, ovf2, poolovf, maxdeg
   uint64_t *start = scratch_raw<uint64_t>(c, nn, &st);
@@ -345,7 +345,9 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
                  dim3(256), 0, (const uint64_t *)g->edge_off, g->E, misc));
   uint64_t T = 0;
   HGP_TRY(read_u64(c, (const uint64_t *)misc, &T));
-  uint64_t pool_cap = T < 24 * g->P + nn ? T : 24 * g->P + nn;
+  // T bounds the total exactly (|N(n)| <= sum over I(n) of (|e| - 1)); a smaller estimate makes
+  // power-law inputs (V ~ T) pay a second full pass. At most 2^34 entries; beyond, the retry.
+  uint64_t pool_cap = T + nn < (1ull << 34) ? T + nn : (1ull << 34);
   if (pool_cap == 0) pool_cap = 1;
   uint32_t *pool = scratch_raw<uint32_t>(c, pool_cap, &st);
   if (st) return st;

@@ -66,36 +66,49 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
     uint64_t g = 1;
     uint32_t ib = 0;
     if (MODE == kModeP32) {
-      uint64_t sum = 0, gg = 0;
+      // S1 first; the gcd of c(e) (a binary-GCD reduction: thousands of instructions) only when
+      // g = 1 leaves the packed form inexact
+      uint64_t sum = 0;
       for (uint64_t k = i0 + tid; k < i1; k += THREADS) {
         const uint32_t e = J.inc[k];
-        const uint64_t a = J.edge_off[e], b = J.edge_off[e + 1];
-        const uint64_t ce = edge_c(J, e, a, b);
-        sum += ce;
-        gg = gcd64(gg, ce);
+        sum += edge_c(J, e, J.edge_off[e], J.edge_off[e + 1]);
       }
+      sum = warp_sum(sum);
+      if (lane == 0) s_sum[w] = sum;
+      __syncthreads();
+      uint64_t S1 = 0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-        gg = gcd64(gg, __shfl_xor_sync(0xFFFFFFFFu, gg, o));
+      for (uint32_t q = 0; q < NW; ++q) S1 += s_sum[q];
+      const uint32_t bits = inn ? 32 - __clz(inn) : 0;
+      if ((((unsigned __int128)(S1 + 1)) << bits) <= ((unsigned __int128)1 << 32)) {   // CTA-uniform
+        g = 1;
+        ib = bits;
+        __syncthreads();                                          // s_sum is rewritten next node
+      } else {
+        uint64_t gg = 0;
+        for (uint64_t k = i0 + tid; k < i1; k += THREADS) {
+          const uint32_t e = J.inc[k];
+          gg = gcd64(gg, edge_c(J, e, J.edge_off[e], J.edge_off[e + 1]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) gg = gcd64(gg, __shfl_xor_sync(0xFFFFFFFFu, gg, o));
+        if (lane == 0) s_g[w] = gg;
+        __syncthreads();
+        if (tid == 0) {
+          uint64_t G1 = 0;
+          for (uint32_t q = 0; q < NW; ++q) G1 = gcd64(G1, s_g[q]);
+          if (G1 == 0) G1 = 1;
+          const unsigned __int128 need = ((unsigned __int128)(S1 / G1 + 1)) << bits;
+          s_defer = need > ((unsigned __int128)1 << 32);
+          s_gcd = G1;
+          s_ib = bits;
+          if (s_defer) J.wide_list[atomicAdd(J.wide_count, 1u)] = n;
+        }
+        __syncthreads();
+        if (s_defer) continue;                                    // CTA-uniform
+        g = s_gcd;
+        ib = s_ib;
       }
-      if (lane == 0) { s_sum[w] = sum; s_g[w] = gg; }
-      __syncthreads();
-      if (tid == 0) {
-        uint64_t S1 = 0, G1 = 0;
-        for (uint32_t q = 0; q < NW; ++q) { S1 += s_sum[q]; G1 = gcd64(G1, s_g[q]); }
-        if (G1 == 0) G1 = 1;
-        const uint32_t bits = inn ? 32 - __clz(inn) : 0;
-        const unsigned __int128 need = ((unsigned __int128)(S1 / G1 + 1)) << bits;
-        s_defer = need > ((unsigned __int128)1 << 32);
-        s_gcd = G1;
-        s_ib = bits;
-        if (s_defer) J.wide_list[atomicAdd(J.wide_count, 1u)] = n;
-      }
-      __syncthreads();
-      if (s_defer) continue;                                      // CTA-uniform
-      g = s_gcd;
-      ib = s_ib;
     }
     if (MODE == kModeSplit) {                                     // eta fits u32 iff sum c(e) < 2^32
       uint64_t sum = 0;
@@ -153,7 +166,7 @@ __global__ void __launch_bounds__(THREADS) k_score(ScoreJob J) {
       }
       uint32_t add_s = 0, add_d = 0;
       if (MODE == kModeP32) {
-        add_s = (uint32_t)((ce / g) << ib);
+        add_s = (uint32_t)((g == 1 ? ce : ce / g) << ib);
         add_d = add_s + mu_in;                                     // m in dst(e) and e in in(n)
       } else if (MODE == kModeSplit) {
         add_s = (uint32_t)ce;                                      // eta term

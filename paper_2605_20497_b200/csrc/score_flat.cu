@@ -114,8 +114,12 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
     for (uint32_t q = 0; q < NW; ++q) S1 += s_sum[q];
     uint32_t ib = 0;
     bool packed;
+    const uint32_t ib0 = nointer || !inn ? 0 : 32 - __clz(inn);
     if (nointer && S1 < (1ull << 32)) {
       packed = true;                                                 // acc = eta itself
+    } else if (ib0 < 32 && S1 + 1 <= (1ull << (32 - ib0))) {
+      packed = true;                                                 // g = 1 already fits: no gcd
+      ib = ib0;
     } else {
       // gcd of c(e) over I(n): (eta / g) << ib | inter fits 32 bits more often
       uint64_t gg = tce;
@@ -176,7 +180,7 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
           mu = !nointer && t0 + tid < iin ? J.edge_mu[e] : 0u;
         }
         if (packed) {
-          as = (uint32_t)((ce == g ? 1ull : ce / g) << ib);
+          as = (uint32_t)((ce == g ? 1ull : g == 1 ? ce : ce / g) << ib);
           ad = as + mu;                                             // m in dst(e), e in in(n)
         } else {
           as = (uint32_t)ce;                                        // eta term

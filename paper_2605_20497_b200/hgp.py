@@ -264,7 +264,7 @@ class Ctx:
         _check(lib().hgp_sync(self.h))
 
     OPTION_DEFAULTS = {"fused_sample_min": 65536, "fused_pool_cap": 0, "unfused": 0, "inc_radix": 0,
-                       "debug_sync": 0}
+                       "debug_sync": 0, "no_hub": 0}
 
     def set_option(self, name: str, value: int):
         """hgp_ctx_set_option (tests / experiments; results never depend on options)."""
@@ -303,7 +303,7 @@ class Ctx:
 
     TIERS = ["fused_S", "fused_A", "fused_M", "fused_B", "nbrs_1", "nbrs_2", "nbrs_3", "score_nointer",
              "score_packed", "score_split", "score_B", "score_W", "score_H", "cnbrs_A", "cnbrs_M", "cnbrs_B",
-             "cnbrs_C", "jump", "fused_W"]
+             "cnbrs_C", "jump", "fused_W", "fused_H", "cnbrs_H", "cnbrs_A2"]
 
     def tier_counts(self, reset: bool = False) -> dict:
         """hgp_tier_counts: nodes processed per kernel tier (include/hgp.h HGP_TIER_*)."""

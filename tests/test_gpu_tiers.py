@@ -76,7 +76,9 @@ def test_unfused_hub_tiers(hgp, ctx):
     """a2 tiers 1-3, a3 first tier and B, a5 coarse neighbour tiers A-C: edges of 20000, 7000, 3000
     and 1500 pins among many small ones."""
     ctx.tier_counts(reset=True)
-    _unfused_level(hgp, ctx, _hubs(0, 30000, [17500, 7000, 3000, 1500, 40, 2]), 8, 10 ** 6)
+    _unfused_level(hgp, ctx, _hubs(0, 30000, [17500, 7000, 3000, 1500, 40, 2]), 8, 10 ** 6)   # a5 hubs: tier H
+    with ctx.options(no_hub=1):                        # a5 hubs (bounds ~18000): the global-memory tier C
+        _unfused_level(hgp, ctx, _hubs(7, 12000, [9000, 40, 2], small=1000), 8, 10 ** 6)
     _record(ctx)
 
 
@@ -103,11 +105,15 @@ def test_score_modes(hgp, ctx):
 
 def test_fused_tiers(hgp, ctx):
     """The fused level-0 kernel: the sampled first tier, A, M (neighbourhoods of ~2800 through the
-    sampling decision) and B (a 6000-pin edge: neighbourhoods above M's 4096)."""
+    sampling decision), B (a 6000-pin edge: neighbourhoods above M's 4096) and the hub tier (edges
+    of 8700-9500 pins; weights up to 400 and a tight Delta: gcd and inter in the packed term)."""
     ctx.tier_counts(reset=True)
     cases = [(hgpgen.snn(8, layers=4, rows=40, cols=60, fanout=99, window=15, rewire=1.0), 256, 4096, 128),
              (hgpgen.snn(6, layers=3, rows=30, cols=30, fanout=60, window=11), 64, 4096, 128),
-             (_hubs(3, 20000, [6000, 40], small=2000, wmax=1), 8, 10 ** 6, 65536)]
+             (_hubs(3, 20000, [6000, 40], small=2000, wmax=1), 8, 10 ** 6, 65536),
+             # hubs: b(n) > 8192 pin visits -> the key-partitioned hub tier (8 partitions per node)
+             (_hubs(5, 20000, [9000, 40], small=2000, wmax=1), 8, 10 ** 6, 65536),
+             (_hubs(6, 20000, [9500, 8700], small=2000, wmax=400), 8, 40, 65536)]
     for hg, omega, delta, smin in cases:
         with ctx.options(fused_sample_min=smin):
             cap = hgpgen.default_noise_cap(hg)
@@ -125,6 +131,22 @@ def test_fused_tiers(hgp, ctx):
             assert_cand_equal(hgp.cand_to_numpy(cand), rr["cand"])
             assert np.array_equal(m.cpu().numpy(), rr["match"])
             assert_csr_equal(cg.to_host(), rr["coarse"], "fused coarse")
+            assert_nbrs_equal(cnb.to_host(), rr["coarse_nb"], "fused coarse nbrs")
+            # the bench's form: N(n) left in the fused pool, N'(c) written over it in place
+            cand2 = hgp.empty_cand(g.N, 4)
+            _, cg2, cnb2, _ = hgp.coarsen_level0(ctx, g, hgp.params(omega, delta, 4, noise_seed=2, noise_cap=cap),
+                                                 cand2, m, gam, want_nbrs=False)
+            assert_cand_equal(hgp.cand_to_numpy(cand2), rr["cand"])
+            assert_csr_equal(cg2.to_host(), rr["coarse"], "fused coarse (in place)")
+            assert_nbrs_equal(cnb2.to_host(), rr["coarse_nb"], "fused coarse nbrs (in place)")
+            if hg.num_nodes == 20000 and omega == 8 and delta == 40:
+                # hubs on the unfused list path instead (a2 list tiers, a3 list scoring)
+                with ctx.options(no_hub=1):
+                    cand3 = hgp.empty_cand(g.N, 4)
+                    _, cg3, cnb3, _ = hgp.coarsen_level0(ctx, g, hgp.params(omega, delta, 4, noise_seed=2, noise_cap=cap),
+                                                         cand3, m, gam, want_nbrs=False)
+                    assert_cand_equal(hgp.cand_to_numpy(cand3), rr["cand"])
+                    assert_nbrs_equal(cnb3.to_host(), rr["coarse_nb"], "unfused hubs, coarse nbrs")
     _record(ctx)
 
 
