@@ -445,7 +445,13 @@ __global__ void k_cnbr_pack(const uint32_t *pool, const uint64_t *bound_off, con
     const uint32_t n = cnt[c];
     const uint32_t *src = pool + bound_off[c];
     uint32_t *dst = nbr + off[c];
-    for (uint32_t i = lane; i < n; i += 32) dst[i] = src[i];
+    for (uint32_t i0 = 0; i0 < n; i0 += 128) {                    // 4 loads in flight per lane
+      uint32_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { const uint32_t i = i0 + u * 32 + lane; v[u] = i < n ? src[i] : 0u; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { const uint32_t i = i0 + u * 32 + lane; if (i < n) dst[i] = v[u]; }
+    }
     mx = max(mx, n);
   }
   mx = warp_max(mx);
@@ -461,7 +467,16 @@ __global__ void k_cnbr_pack_inplace(CNbrJob J, const uint64_t *off, uint32_t Nc,
     const uint64_t a0 = J.nb_start[a], na = J.nb_len[a];
     const uint64_t b0 = b == kNone ? 0 : J.nb_start[b];
     uint32_t *dst = nbr + off[c];
-    for (uint32_t i = lane; i < n; i += 32) dst[i] = J.nbr_w[i < na ? a0 + i : b0 + (i - na)];
+    for (uint32_t i0 = 0; i0 < n; i0 += 128) {                    // 4 loads in flight per lane
+      uint32_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = i0 + u * 32 + lane;
+        v[u] = i < n ? J.nbr_w[i < na ? a0 + i : b0 + (i - na)] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { const uint32_t i = i0 + u * 32 + lane; if (i < n) dst[i] = v[u]; }
+    }
     mx = max(mx, n);
   }
   mx = warp_max(mx);

@@ -26,7 +26,7 @@ namespace hgp {
 // flat start of dst(e), add of a src pin} and u32 {add of a dst pin}.
 constexpr uint32_t kKT = 128;     // incident edges per tile
 constexpr uint32_t fused_smem(uint32_t lg) { return (12u << lg) + kKT * 20u; }
-constexpr uint32_t fused_smem_list(uint32_t lg) { return (9u << lg) + kKT * 20u; }   // keys, acc, u16 list
+constexpr uint32_t fused_smem_list(uint32_t lg) { return (9u << lg) + (lg >= 13 ? 64u : kKT) * 20u; }   // keys, acc, u16 list
 
 // predicated shared CAS: lanes with p == false return `dflt` without touching memory
 __device__ __forceinline__ uint32_t cas_u32_if(bool p, uint32_t a, uint32_t cmp, uint32_t val, uint32_t dflt) {
@@ -63,7 +63,10 @@ template <int THREADS, int PIMAX, int MINB, int LOG2S, bool LIST = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
   extern __shared__ __align__(16) unsigned char dyn[];
   constexpr uint32_t NW = THREADS / 32;
-  static_assert(THREADS >= (int)kKT, "one edge row per thread");
+  // incident edges per tile: 64 in M's LIST form (its 74.5 KB then fits 3 CTAs per SM, with the
+  // 1 KB per-CTA reservation), kKT elsewhere
+  constexpr uint32_t KT = (LIST && LOG2S >= 13) ? 64u : kKT;
+  static_assert(THREADS >= (int)KT, "one edge row per thread");
   __shared__ uint64_t s_tops[(NW + 1) * PIMAX];
   __shared__ uint32_t s_topi[(NW + 1) * PIMAX];
   __shared__ uint64_t s_sum[NW], s_g[NW];
@@ -79,10 +82,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
   uint16_t *slist = reinterpret_cast<uint16_t *>(acc + S);         // (LIST: ucap slots)
   static_assert(!LIST || S <= 65536, "u16 slot list");
   uint4 *rows = LIST ? reinterpret_cast<uint4 *>(slist + S / 2) : reinterpret_cast<uint4 *>(dense + S / 2);
-  uint32_t *rowd = reinterpret_cast<uint32_t *>(rows + kKT);
+  uint32_t *rowd = reinterpret_cast<uint32_t *>(rows + KT);
   // shared-window addresses kept in registers (no rematerialisation inside the pin loop)
   const uint32_t keys_s = opaque_u32(smem_u32addr(keys)), acc_s = keys_s + 4 * S;
-  const uint32_t rows_s = opaque_u32(smem_u32addr(rows)), rowd_s = rows_s + 16 * kKT;
+  const uint32_t rows_s = opaque_u32(smem_u32addr(rows)), rowd_s = rows_s + 16 * KT;
   const uint32_t total = F.list_count ? *F.list_count : J.hi - J.lo;
   const bool unb = J.delta == HGP_UNBOUNDED;
   const uint64_t mxin = J.max_in_mu ? *J.max_in_mu : 0xFFFFFFFFull;   // max in_mu of the level
@@ -102,7 +105,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
     // and with a uniform c(e) every pin visit adds exactly 1 (the ADD1 pin loop)
     const bool noint = unb || (uint64_t)inn + mxin <= J.delta;
     // ---- prologue: the first tile's edge data stays in registers
-    const bool mine = tid < kKT && i0 + tid < i1;
+    const bool mine = tid < KT && i0 + tid < i1;
     uint32_t tlen = 0, tns = 0, tmu = 0;
     uint64_t ta = 0, tce = 0;
     if (mine) {
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
     bool diff = mine && tce != c0;
     uint64_t sum = tce;                                            // S1 = sum of c(e), published with B1
 #pragma unroll 1
-    for (uint64_t k = i0 + kKT + tid; k < i1; k += THREADS) {
+    for (uint64_t k = i0 + KT + tid; k < i1; k += THREADS) {
       const uint64_t ce = F.cv[J.inc[k]];
       diff |= ce != c0;
       sum += ce;
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       if ((((unsigned __int128)(S1 + 1)) << ib0) > ((unsigned __int128)1 << 32)) {
         uint64_t gg = tce;
 #pragma unroll 1
-        for (uint64_t k = i0 + kKT + tid; k < i1; k += THREADS) gg = gcd64(gg, F.cv[J.inc[k]]);
+        for (uint64_t k = i0 + KT + tid; k < i1; k += THREADS) gg = gcd64(gg, F.cv[J.inc[k]]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           const uint64_t og = __shfl_xor_sync(0xFFFFFFFFu, gg, o);
@@ -177,8 +180,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
     if (tid == 0) keys[hash_slot(n, LOG2S)] = n;                  // the table is clean: n's home; self-visits land there
     // ---- phase 1, tile by tile
     bool full = false;
-    for (uint64_t t0 = i0; t0 < i1; t0 += kKT) {
-      const uint32_t kt = (uint32_t)min((uint64_t)kKT, i1 - t0);
+    for (uint64_t t0 = i0; t0 < i1; t0 += KT) {
+      const uint32_t kt = (uint32_t)min((uint64_t)KT, i1 - t0);
       uint32_t len = tlen, ns = tns, mu = tmu, incl = tincl;
       uint64_t a = ta, ce = tce;
       if (t0 != i0) {
@@ -355,12 +358,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
       uint4 ra = lds_v4(rows_s + 16 * k);
       uint32_t rd = lds_u32(rowd_s + 4 * k);
       // one 128-pin window of this warp's flat range; FULL: the window lies inside [flo, fhi)
-      // ADD1: every visit adds 1 (noint, uniform c(e)): only (row end, pins base) are tracked
-      auto window = [&](uint32_t f0, auto full_tag, auto long_tag, auto add1_tag) {
+      // ADD1: every visit adds 1 (noint, uniform c(e)): only (row end, pins base) are tracked.
+      // fetch: the window's 4 pins per lane (row advance, pin loads); window = fetch + insert4.
+      auto fetch = [&](uint32_t f0, uint32_t (&m)[4], uint32_t (&add)[4], bool (&val)[4], auto full_tag, auto long_tag,
+                       auto add1_tag) {
         constexpr bool FULL = decltype(full_tag)::value, LONG = decltype(long_tag)::value;
         constexpr bool ADD1 = decltype(add1_tag)::value;
-        uint32_t m[4], add[4];
-        bool val[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t f = f0 + u * 32 + lane;
@@ -410,6 +413,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
           m[u] = val[u] ? __ldg(J.pins + (ra.y + f)) : 0u;
           add[u] = ADD1 ? 1u : (f >= ra.z ? rd : ra.w);
         }
+      };
+      auto window = [&](uint32_t f0, auto full_tag, auto long_tag, auto add1_tag) {
+        uint32_t m[4], add[4];
+        bool val[4];
+        fetch(f0, m, add, val, full_tag, long_tag, add1_tag);
         insert4(m, add, val, full_tag);
       };
       uint32_t f0 = flo;
@@ -545,7 +553,13 @@ __global__ void k_fused_pack(const uint32_t *pool, const uint64_t *start, const 
     const uint32_t c = cnt[t];
     const uint32_t *src = pool + start[t];
     uint32_t *dst = nbr + off[t];
-    for (uint32_t j = lane; j < c; j += 32) dst[j] = src[j];
+    for (uint32_t j0 = 0; j0 < c; j0 += 128) {                    // 4 loads in flight per lane
+      uint32_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { const uint32_t j = j0 + u * 32 + lane; v[u] = j < c ? src[j] : 0u; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { const uint32_t j = j0 + u * 32 + lane; if (j < c) dst[j] = v[u]; }
+    }
     mx = max(mx, c);
   }
   mx = warp_max(mx);
