@@ -392,7 +392,7 @@ def main():
     dominant = args.dominant or max(breakdown, key=lambda k: breakdown[k][0])
     # the dominant kernel's family (every tier launch of it in a step, e.g. nbrscore_S/A/M/B):
     # the step's algorithmic work is charged to their summed device time
-    family = dominant.split("_")[0] if dominant.split("_")[-1] in ("S", "A", "M", "B", "W", "H", "C") else dominant
+    family = dominant.rsplit("_", 1)[0] if dominant.split("_")[-1] in ("S", "A", "M", "B", "W", "H", "C", "A2") else dominant
 
     # ---- timed region: K steps, inputs resident in HBM (420 MB > 126 MB L2)
     clocks = ClockSampler(local)

@@ -826,6 +826,10 @@ __global__ void __launch_bounds__(kWWarps * 32) k_nbrscore_w(FusedJob F) {
 // accumulator cannot represent) goes to the unfused kernels.
 static constexpr int kFALog = 12, kFMLog = 13, kFBLog = 14;
 static constexpr uint32_t kFMThreads = 256, kFBThreads = 256;
+// A's LIST form (routed power-law nodes, ~1,000 visits each): 4 warps per node, 5 nodes per SM —
+// per-node latency (dependent loads, barriers) bounds these nodes, so nodes in flight count more
+// than warps per node
+static constexpr uint32_t kFALThreads = 128;
 
 struct TierLists {
   const uint32_t *in_list, *in_count;   // nullptr: every node of [lo, hi)
@@ -846,7 +850,7 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
                          fused_smem(kFMLog));
     cudaFuncSetAttribute(k_nbrscore<kFBThreads, PIMAX, 1, kFBLog>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          fused_smem(kFBLog));
-    cudaFuncSetAttribute(k_nbrscore<TA, PIMAX, MINB, kFALog, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_nbrscore<kFALThreads, PIMAX, 5, kFALog, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          fused_smem_list(kFALog));
     cudaFuncSetAttribute(k_nbrscore<kFMThreads, PIMAX, 3, kFMLog, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          fused_smem_list(kFMLog));
@@ -907,7 +911,10 @@ hgp_status fused_tiers_t(hgp_ctx *c, FusedJob F, const TierLists &L) {
     F.list = L.in_list; F.list_count = L.in_count; F.log2s = kFALog; F.tier = HGP_TIER_FUSED_A;
     F.defer_list = L.la; F.defer_count = L.ca;
     if (L.list_mode)
-      HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog, true>, dim3(gA), dim3(TA),
+      HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<kFALThreads, PIMAX, 5, kFALog, true>,
+                     dim3(std::min(L.hn, resident_grid(c, k_nbrscore<kFALThreads, PIMAX, 5, kFALog, true>, kFALThreads,
+                                                        fused_smem_list(kFALog)))),
+                     dim3(kFALThreads),
                      fused_smem_list(kFALog), F));
     else
       HGP_TRY(launch(c, "nbrscore_A", k_nbrscore<TA, PIMAX, MINB, kFALog>, dim3(gA), dim3(TA), fused_smem(kFALog), F));
