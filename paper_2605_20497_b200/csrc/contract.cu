@@ -313,7 +313,8 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
       __syncthreads();
     }
     // 4 entries per thread in flight: nbr loads, then the gamma gathers, then the inserts
-    for (uint64_t k0 = tid; k0 < na + nbn; k0 += 4 * THREADS) {
+    for (uint64_t kb = 0; kb < na + nbn; kb += 4 * THREADS) {       // CTA-uniform trip count
+      const uint64_t k0 = kb + tid;
       uint32_t v[4], gm[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -322,6 +323,7 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) gm[u] = v[u] != kEmpty ? __ldg(J.gamma + (v[u] & kIdMask)) : kEmpty;
+      uint32_t nslot[4], newm = 0;                                  // new keys: slots, mask (SMEM)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (v[u] == kEmpty) continue;
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
           while (true) {
             if (k == kEmpty) {
               k = cas_u32(keys_s + 4 * slot, kEmpty, fl ? (gm[u] | kPurge) : gm[u]);
-              if (k == kEmpty) { slist[atomicAdd(&s_n, 1u)] = (uint16_t)slot; break; }   // a new key
+              if (k == kEmpty) { nslot[u] = slot; newm |= 1u << u; break; }   // a new key
             }
             if ((k & kIdMask) == gm[u]) {
               if (fl && !(k & kPurge)) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(keys_s + 4 * slot), "r"(kPurge) : "memory");
@@ -346,6 +348,16 @@ __global__ void __launch_bounds__(THREADS) k_coarse_nbrs(CNbrJob J) {
           uint32_t slot;
           hs_insert_flagged(keys, nlog, gm[u], fl, &slot);
         }
+      }
+      if constexpr (SMEM) {   // the new keys' slots to the list: one shared atomic per warp
+        const uint32_t nnew = __popc(newm);
+        const uint32_t incl = warp_incl_scan(nnew);
+        uint32_t base = 0;
+        if (lane == 31 && incl) base = atomicAdd(&s_n, incl);
+        base = __shfl_sync(0xFFFFFFFFu, base, 31) + incl - nnew;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if ((newm >> u) & 1u) slist[base + __popc(newm & ((1u << u) - 1))] = (uint16_t)nslot[u];
       }
     }
     __syncthreads();
