@@ -102,20 +102,32 @@ __device__ __forceinline__ void eval_packed(const ScoreJob &J, const FusedJob &F
   uint64_t carry = 0;                                              // lane r < pi: the warp's r-th best
   for (uint32_t c0 = w * 32; c0 < count; c0 += 4 * THREADS) {     // warp-uniform
     uint64_t k[4];
+    uint2 d[4], wm[4];
+    // the 4 entries, then their 4 (size, in_mu) gathers in flight together, then the tests
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = c0 + u * THREADS + lane;
+      d[u] = i < count ? dense[i] : make_uint2(kEmpty, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) wm[u] = d[u].x != kEmpty ? __ldg(F.wmu + d[u].x) : make_uint2(0u, 0u);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t i = c0 + u * THREADS + lane;
       k[u] = 0;
-      if (i < count) {
-        const uint2 d = dense[i];
-        uint32_t cnt;
-        if (eval_one(F, E, d, base + i, cnt)) {
+      if (d[u].x != kEmpty) {
+        const uint32_t v = d[u].x, x = d[u].y;
+        const uint32_t cnt = E.ib < 32 ? x >> E.ib : 0u;
+        // |in(n) ∪ in(m)| = in_mu(n) + in_mu(m) - inter; inter <= in_mu(m)
+        const bool ok = E.wn + wm[u].x <= E.om32 && E.inn + (wm[u].y - (x & E.imask)) <= E.de32;
+        F.pool[base + i] = ok ? v : (v | kPurge);                  // purge flag
+        if (ok) {
           uint32_t s32 = cnt * g32;                                // eta(n, m) < 2^32
           if (cap32) {
-            const uint64_t key = ((uint64_t)min(n, d.x) << 32) | max(n, d.x);
+            const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
             s32 += (uint32_t)__umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);   // uniform in [0, cap]
           }
-          k[u] = ((uint64_t)s32 << 32) | d.x;
+          k[u] = ((uint64_t)s32 << 32) | v;
         }
       }
     }

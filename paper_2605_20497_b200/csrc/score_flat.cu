@@ -306,93 +306,116 @@ __global__ void __launch_bounds__(kFThreads, 4) k_score_flat(ScoreJob J, const u
     if (i1 == i0) __syncthreads();                                  // phase 1's inserts before phase 3
     // ---- phase 3: validity (Eq.6), flags, noise, top-pi
     const bool small = (unsigned __int128)S1 + J.noise_cap < ((unsigned __int128)1 << 32);   // keys (score << 32 | id)
-    TopK<PIMAX> topk;
-    Top<PIMAX> top;
-#pragma unroll
-    for (int q = 0; q < PIMAX; ++q) { topk.k[q] = 0; top.s[q] = 0; top.id[q] = 0; }
-    uint64_t thr = 0;
     const uint64_t wn = J.node_w[n];
     const uint32_t imask = ib ? (uint32_t)((1ull << ib) - 1) : 0u;
-    for (uint32_t i = tid; i < cnt; i += kFThreads) {
-      const uint32_t sl = nslot[i];
-      if (sl == 0xFFFFu) continue;                                  // already purged
-      const uint32_t v = keys[sl];
-      uint64_t e_nm, it;
-      if (packed) {
-        const uint32_t x = acc[sl];
-        e_nm = (uint64_t)(ib < 32 ? x >> ib : 0) * g;
-        it = x & imask;
-      } else {
-        e_nm = acc[sl];
-        it = (inter[sl >> 1] >> (16 * (sl & 1))) & 0xFFFFu;
-      }
-      const uint2 wm = __ldg(wmu + v);                               // (size(m), in_mu(m))
-      const uint64_t uni = (uint64_t)inn + wm.y - it;                // |in(n) ∪ in(m)|
-      const bool ok = wn + wm.x <= J.omega && (J.delta == HGP_UNBOUNDED || uni <= J.delta);
-      if (!ok) { J.nbr[b0 + i] = v | kPurge; continue; }
-      if (small && ((((e_nm + J.noise_cap) << 32) | v) <= thr)) continue;   // cannot enter the top-pi
-      uint64_t sc = e_nm;
-      if (J.noise_cap) {
-        const uint64_t key = ((uint64_t)min(n, v) << 32) | max(n, v);
-        sc += __umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);    // uniform in [0, cap]
-      }
-      if (small) {
-        const uint64_t key = (sc << 32) | v;
-        if (key > thr) {
-          topk_insert<PIMAX>(topk, J.pi, key);
+    // SMALL: (score << 32 | id) u64 keys with a running threshold; else (u64 score, id) lists.
+    // Two instantiations, so only one list is live.
+    auto phase3 = [&](auto small_tag) {
+      constexpr bool SMALL = decltype(small_tag)::value;
+      TopK<PIMAX> topk;
+      Top<PIMAX> top;
 #pragma unroll
-          for (int q = 0; q < PIMAX; ++q)
-            if (q == (int)J.pi - 1) thr = topk.k[q];
-        }
-      } else {
-        top_insert<PIMAX>(top, J.pi, sc, v);
+      for (int q = 0; q < PIMAX; ++q) {
+        if (SMALL) topk.k[q] = 0;
+        else { top.s[q] = 0; top.id[q] = 0; }
       }
-    }
-    // ---- phase 4: merges (warps, then warp 0)
-    if (small) warp_topk_merge<PIMAX>(topk, J.pi, s_tops + w * PIMAX);
-    else warp_top_merge<PIMAX>(top, J.pi, s_tops + w * PIMAX, s_topi + w * PIMAX);
+      uint64_t thr = 0;
+      // 2 entries per thread in flight: slots, then their (size, in_mu) gathers together; each
+      // thread clears the slots it read (no separate reset pass over the list)
+      for (uint32_t i0 = tid; i0 < cnt; i0 += 2 * kFThreads) {
+        uint32_t sl[2], v[2], x[2], xi[2];
+        uint2 wm[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t i = i0 + u * kFThreads;
+          sl[u] = i < cnt ? nslot[i] : 0xFFFFu;
+          v[u] = kEmpty; x[u] = 0; xi[u] = 0;
+          if (sl[u] != 0xFFFFu) {
+            v[u] = keys[sl[u]];
+            x[u] = acc[sl[u]];
+            if (!packed) xi[u] = (inter[sl[u] >> 1] >> (16 * (sl[u] & 1))) & 0xFFFFu;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) wm[u] = sl[u] != 0xFFFFu ? __ldg(wmu + v[u]) : make_uint2(0u, 0u);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (sl[u] == 0xFFFFu) continue;                           // already purged (or past cnt)
+          keys[sl[u]] = kEmpty; acc[sl[u]] = 0; inter[sl[u] >> 1] = 0;   // both halves are ours to clear
+          uint64_t e_nm, it;
+          if (packed) {
+            e_nm = (uint64_t)(ib < 32 ? x[u] >> ib : 0) * g;
+            it = x[u] & imask;
+          } else {
+            e_nm = x[u];
+            it = xi[u];
+          }
+          const uint64_t uni = (uint64_t)inn + wm[u].y - it;        // |in(n) ∪ in(m)|
+          const bool ok = wn + wm[u].x <= J.omega && (J.delta == HGP_UNBOUNDED || uni <= J.delta);
+          if (!ok) { J.nbr[b0 + i0 + u * kFThreads] = v[u] | kPurge; continue; }
+          if (SMALL && ((((e_nm + J.noise_cap) << 32) | v[u]) <= thr)) continue;   // cannot enter the top-pi
+          uint64_t sc = e_nm;
+          if (J.noise_cap) {
+            const uint64_t key = ((uint64_t)min(n, v[u]) << 32) | max(n, v[u]);
+            sc += __umul64hi(splitmix64(key ^ J.seed_mix), J.noise_cap + 1);    // uniform in [0, cap]
+          }
+          if (SMALL) {
+            const uint64_t key = (sc << 32) | v[u];
+            if (key > thr) {
+              topk_insert<PIMAX>(topk, J.pi, key);
+#pragma unroll
+              for (int q = 0; q < PIMAX; ++q)
+                if (q == (int)J.pi - 1) thr = topk.k[q];
+            }
+          } else {
+            top_insert<PIMAX>(top, J.pi, sc, v[u]);
+          }
+        }
+      }
+      // ---- phase 4: merges (warps, then warp 0)
+      if (SMALL) warp_topk_merge<PIMAX>(topk, J.pi, s_tops + w * PIMAX);
+      else warp_top_merge<PIMAX>(top, J.pi, s_tops + w * PIMAX, s_topi + w * PIMAX);
+      __syncthreads();
+      if (w == 0) {
+        if (SMALL) {
+          TopK<PIMAX> t2;
+#pragma unroll
+          for (int q = 0; q < PIMAX; ++q) t2.k[q] = 0;
+          for (uint32_t i = lane; i < NW * J.pi; i += 32) topk_insert<PIMAX>(t2, J.pi, s_tops[(i / J.pi) * PIMAX + i % J.pi]);
+          warp_topk_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX);
+          __syncwarp();
+          for (uint32_t r = lane; r < J.pi; r += 32) {
+            const uint64_t kx = s_tops[NW * PIMAX + r];
+            hgp_cand cd;
+            cd.score = kx >> 32;
+            cd.id = kx ? (uint32_t)kx : kNone;
+            cd.pad = 0;
+            J.cand[(uint64_t)n * J.pi + r] = cd;
+          }
+        } else {
+          Top<PIMAX> t2;
+#pragma unroll
+          for (int q = 0; q < PIMAX; ++q) { t2.s[q] = 0; t2.id[q] = 0; }
+          for (uint32_t i = lane; i < NW * J.pi; i += 32) {
+            const uint32_t ww = i / J.pi, r = i % J.pi;
+            top_insert<PIMAX>(t2, J.pi, s_tops[ww * PIMAX + r], s_topi[ww * PIMAX + r]);
+          }
+          warp_top_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX, s_topi + NW * PIMAX);
+          __syncwarp();
+          for (uint32_t r = lane; r < J.pi; r += 32) {
+            hgp_cand cd;
+            cd.score = s_tops[NW * PIMAX + r];
+            cd.id = cd.score ? s_topi[NW * PIMAX + r] : kNone;
+            cd.pad = 0;
+            J.cand[(uint64_t)n * J.pi + r] = cd;
+          }
+        }
+      }
+    };
+    if (small) phase3(std::true_type{});
+    else phase3(std::false_type{});
     __syncthreads();
-    if (w == 0) {
-      if (small) {
-        TopK<PIMAX> t2;
-#pragma unroll
-        for (int q = 0; q < PIMAX; ++q) t2.k[q] = 0;
-        for (uint32_t i = lane; i < NW * J.pi; i += 32) topk_insert<PIMAX>(t2, J.pi, s_tops[(i / J.pi) * PIMAX + i % J.pi]);
-        warp_topk_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX);
-        __syncwarp();
-        for (uint32_t r = lane; r < J.pi; r += 32) {
-          const uint64_t kx = s_tops[NW * PIMAX + r];
-          hgp_cand cd;
-          cd.score = kx >> 32;
-          cd.id = kx ? (uint32_t)kx : kNone;
-          cd.pad = 0;
-          J.cand[(uint64_t)n * J.pi + r] = cd;
-        }
-      } else {
-        Top<PIMAX> t2;
-#pragma unroll
-        for (int q = 0; q < PIMAX; ++q) { t2.s[q] = 0; t2.id[q] = 0; }
-        for (uint32_t i = lane; i < NW * J.pi; i += 32) {
-          const uint32_t ww = i / J.pi, r = i % J.pi;
-          top_insert<PIMAX>(t2, J.pi, s_tops[ww * PIMAX + r], s_topi[ww * PIMAX + r]);
-        }
-        warp_top_merge<PIMAX>(t2, J.pi, s_tops + NW * PIMAX, s_topi + NW * PIMAX);
-        __syncwarp();
-        for (uint32_t r = lane; r < J.pi; r += 32) {
-          hgp_cand cd;
-          cd.score = s_tops[NW * PIMAX + r];
-          cd.id = cd.score ? s_topi[NW * PIMAX + r] : kNone;
-          cd.pad = 0;
-          J.cand[(uint64_t)n * J.pi + r] = cd;
-        }
-      }
-    }
-    __syncthreads();
-    // ---- reset the used slots
-    for (uint32_t i = tid; i < cnt; i += kFThreads) {
-      const uint32_t sl = nslot[i];
-      if (sl != 0xFFFFu) { keys[sl] = kEmpty; acc[sl] = 0; inter[sl >> 1] = 0; }   // both halves are ours to clear
-    }
+    // (the listed slots were cleared by the threads that read them)
     if (tid == 0) { keys[s_self] = kEmpty; acc[s_self] = 0; inter[s_self >> 1] = 0; acc[S] = 0; inter[S / 2] = 0; }
   }
   if (tid == 0) {
