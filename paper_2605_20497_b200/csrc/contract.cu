@@ -449,50 +449,56 @@ __global__ void k_list_max_bound(const uint64_t *bound_off, const uint32_t *list
   if (lane_id() == 0 && mx) atomicMax(maxb, (unsigned long long)mx);
 }
 
-__global__ void k_cnbr_pack(const uint32_t *pool, const uint64_t *bound_off, const uint32_t *cnt, const uint64_t *off,
-                            uint32_t Nc, uint32_t *nbr, unsigned int *maxdeg) {
+// The pack as a flat copy balanced by entries, not by node: warp w copies the output positions
+// [Vc w / W, Vc (w+1) / W), walking the coarse nodes they span (one binary search over off for the
+// first). A warp per node left the hubs' ~10^6-entry neighbourhoods to single warps (C4: 9.4 ms for
+// ~10 GB). INPLACE: N'(c) is the first cnt[c] entries of N(a)'s segment followed by N(b)'s;
+// else the oversized pool slot at bound_off[c].
+template <bool INPLACE>
+__global__ void k_cnbr_pack_flat(CNbrJob J, const uint32_t *pool, const uint64_t *bound_off, const uint64_t *off,
+                                 uint32_t Nc, uint64_t Vc, uint32_t *nbr, unsigned int *maxdeg) {
   const uint32_t lane = lane_id();
-  uint32_t mx = 0;
-  for (uint32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < Nc; c += gridDim.x * (blockDim.x >> 5)) {
-    const uint32_t n = cnt[c];
-    const uint32_t *src = pool + bound_off[c];
-    uint32_t *dst = nbr + off[c];
-    for (uint32_t i0 = 0; i0 < n; i0 += 128) {                    // 4 loads in flight per lane
-      uint32_t v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) { const uint32_t i = i0 + u * 32 + lane; v[u] = i < n ? src[i] : 0u; }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) { const uint32_t i = i0 + u * 32 + lane; if (i < n) dst[i] = v[u]; }
-    }
-    mx = max(mx, n);
-  }
+  const uint64_t W = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint32_t mx = 0;                                                  // max |N'(c)|: grid-stride over c
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < Nc; c += gridDim.x * blockDim.x) mx = max(mx, J.cnt[c]);
   mx = warp_max(mx);
-  if (lane == 0) atomicMax(maxdeg, mx);
-}
-
-// in place: N'(c) is the first cnt[c] entries of N(a)'s segment followed by N(b)'s
-__global__ void k_cnbr_pack_inplace(CNbrJob J, const uint64_t *off, uint32_t Nc, uint32_t *nbr, unsigned int *maxdeg) {
-  const uint32_t lane = lane_id();
-  uint32_t mx = 0;
-  for (uint32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < Nc; c += gridDim.x * (blockDim.x >> 5)) {
-    const uint32_t n = J.cnt[c], a = J.mem0[c], b = J.mem1[c];
-    const uint64_t a0 = J.nb_start[a], na = J.nb_len[a];
-    const uint64_t b0 = b == kNone ? 0 : J.nb_start[b];
-    uint32_t *dst = nbr + off[c];
-    for (uint32_t i0 = 0; i0 < n; i0 += 128) {                    // 4 loads in flight per lane
+  if (lane == 0 && mx) atomicMax(maxdeg, mx);
+  const uint64_t lo = Vc * wid / W, hi = Vc * (wid + 1) / W;
+  if (lo >= hi) return;
+  uint32_t a = 0, b = Nc;                                           // last c with off[c] <= lo
+  while (b - a > 1) {
+    const uint32_t m = (a + b) >> 1;
+    if (off[m] <= lo) a = m; else b = m;
+  }
+  uint64_t pos = lo;
+  for (uint32_t c = a; pos < hi; ++c) {
+    const uint64_t s0 = off[c], s1 = off[c + 1];
+    if (s1 <= pos) continue;                                        // (empty nodes)
+    const uint32_t i0 = (uint32_t)(pos - s0), i1 = (uint32_t)((s1 < hi ? s1 : hi) - s0);
+    uint64_t a0 = 0, na = 0, b0 = 0;
+    const uint32_t *src = nullptr;
+    if (INPLACE) {
+      const uint32_t ma = J.mem0[c], mb = J.mem1[c];
+      a0 = J.nb_start[ma];
+      na = J.nb_len[ma];
+      b0 = mb == kNone ? 0 : J.nb_start[mb];
+    } else {
+      src = pool + bound_off[c];
+    }
+    uint32_t *dst = nbr + s0;
+    for (uint32_t j0 = i0; j0 < i1; j0 += 128) {                    // 4 loads in flight per lane
       uint32_t v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const uint32_t i = i0 + u * 32 + lane;
-        v[u] = i < n ? J.nbr_w[i < na ? a0 + i : b0 + (i - na)] : 0u;
+        const uint32_t i = j0 + u * 32 + lane;
+        v[u] = i < i1 ? (INPLACE ? J.nbr_w[i < na ? a0 + i : b0 + (i - na)] : src[i]) : 0u;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) { const uint32_t i = i0 + u * 32 + lane; if (i < n) dst[i] = v[u]; }
+      for (int u = 0; u < 4; ++u) { const uint32_t i = j0 + u * 32 + lane; if (i < i1) dst[i] = v[u]; }
     }
-    mx = max(mx, n);
+    pos = s0 + i1;
   }
-  mx = warp_max(mx);
-  if (lane == 0) atomicMax(maxdeg, mx);
 }
 
 __global__ void k_count_kept(const uint32_t *rep, uint32_t E, uint32_t *out) {
@@ -1002,11 +1008,11 @@ static hgp_status cnbrs_impl(hgp_ctx *c, CNbrJob J, uint32_t clo, uint32_t chi, 
   CN->nbr = dalloc_n<uint32_t>(c, Vc, &st);
   if (st) return st;
   if (Nc && !inplace)
-    HGP_TRY(launch(c, "cnbr_pack", k_cnbr_pack, dim3(grid_n(c, Nc, 8)), dim3(256), 0, (const uint32_t *)pool,
-                   (const uint64_t *)bound_off, (const uint32_t *)ccnt, (const uint64_t *)CN->off, Nc, CN->nbr, maxes));
+    HGP_TRY(launch(c, "cnbr_pack", k_cnbr_pack_flat<false>, dim3(8u * c->sm_count), dim3(256), 0, J, (const uint32_t *)pool,
+                   (const uint64_t *)bound_off, (const uint64_t *)CN->off, Nc, Vc, CN->nbr, maxes));
   if (Nc && inplace)
-    HGP_TRY(launch(c, "cnbr_pack", k_cnbr_pack_inplace, dim3(grid_n(c, Nc, 8)), dim3(256), 0, J,
-                   (const uint64_t *)CN->off, Nc, CN->nbr, maxes));
+    HGP_TRY(launch(c, "cnbr_pack", k_cnbr_pack_flat<true>, dim3(8u * c->sm_count), dim3(256), 0, J, (const uint32_t *)nullptr,
+                   (const uint64_t *)nullptr, (const uint64_t *)CN->off, Nc, Vc, CN->nbr, maxes));
   uint32_t hmax[2];
   HGP_TRY(read_back(c, maxes, 8, hmax));
   CN->max_deg = hmax[0];
