@@ -18,6 +18,7 @@
 #include "scan.cuh"
 #include "score_common.cuh"
 #include "fused.cuh"
+#include "pack.cuh"
 
 namespace hgp {
 
@@ -545,27 +546,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_nbrscore(FusedJob F) {
   if (tid == 0) tier_add(F.tiers, F.tier, done);
 }
 
-__global__ void k_fused_pack(const uint32_t *pool, const uint64_t *start, const uint32_t *cnt, const uint64_t *off,
-                             uint32_t nn, uint32_t *nbr, unsigned int *maxdeg) {
-  const uint32_t lane = lane_id();
-  uint32_t mx = 0;
-  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < nn; t += gridDim.x * (blockDim.x >> 5)) {
-    const uint32_t c = cnt[t];
-    const uint32_t *src = pool + start[t];
-    uint32_t *dst = nbr + off[t];
-    for (uint32_t j0 = 0; j0 < c; j0 += 128) {                    // 4 loads in flight per lane
-      uint32_t v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) { const uint32_t j = j0 + u * 32 + lane; v[u] = j < c ? src[j] : 0u; }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) { const uint32_t j = j0 + u * 32 + lane; if (j < c) dst[j] = v[u]; }
-    }
-    mx = max(mx, c);
-  }
-  mx = warp_max(mx);
-  if (lane == 0) atomicMax(maxdeg, mx);
-}
-
 __global__ void k_pack_wmu(const uint32_t *node_w, const uint32_t *in_mu, uint32_t N, uint2 *wmu,
                            unsigned int *max_in_mu) {
   uint32_t mx = 0;
@@ -1076,9 +1056,8 @@ hgp_status nbrs_score_fused(hgp_ctx *c, const hgp_csr *g, const hgp_params *p, u
   out->nbr = dalloc_n<uint32_t>(c, V, &st);
   if (st) return st;
   unsigned int *d_max = counts + 7;
-  HGP_TRY(launch(c, "fused_pack", k_fused_pack, dim3(nn / 8 + 1 < 16u * c->sm_count ? nn / 8 + 1 : 16u * c->sm_count),
-                 dim3(256), 0, (const uint32_t *)pool, (const uint64_t *)start, (const uint32_t *)cnt,
-                 (const uint64_t *)out->off, nn, out->nbr, d_max));
+  HGP_TRY(launch(c, "fused_pack", k_seg_pack_flat, dim3(8u * c->sm_count), dim3(256), 0, (const uint32_t *)pool,
+                 (const uint64_t *)start, (const uint32_t *)cnt, (const uint64_t *)out->off, nn, V, out->nbr, d_max));
   uint32_t mx = 0;
   HGP_TRY(read_back(c, d_max, 4, &mx));
   out->max_deg = mx;

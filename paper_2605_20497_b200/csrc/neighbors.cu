@@ -5,6 +5,7 @@
 // ids to a pool at an atomically reserved offset; a scan of the counts and a pack give the
 // CSR. Segments are sets (hash order), see include/hgp.h.
 #include "csr_impl.cuh"
+#include "pack.cuh"
 #include "hashset.cuh"
 #include "scan.cuh"
 
@@ -188,19 +189,38 @@ __global__ void k_nbr_bound(const uint64_t *inc_off, const uint32_t *inc, const 
   }
 }
 
-__global__ void k_nbr_pack(const uint32_t *pool, const uint64_t *start, const uint32_t *cnt, const uint64_t *off,
-                           uint32_t nn, uint32_t *nbr, unsigned int *maxdeg) {
+__global__ void k_seg_pack_flat(const uint32_t *pool, const uint64_t *start, const uint32_t *cnt, const uint64_t *off,
+                                uint32_t nn, uint64_t V, uint32_t *nbr, unsigned int *maxdeg) {
   const uint32_t lane = lane_id();
-  uint32_t mx = 0;
-  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < nn; t += gridDim.x * (blockDim.x >> 5)) {
-    const uint32_t c = cnt[t];
-    const uint32_t *src = pool + start[t];
-    uint32_t *dst = nbr + off[t];
-    for (uint32_t j = lane; j < c; j += 32) dst[j] = src[j];
-    mx = max(mx, c);
-  }
+  const uint64_t W = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint32_t mx = 0;                                                  // max segment: grid-stride over t
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nn; t += gridDim.x * blockDim.x) mx = max(mx, cnt[t]);
   mx = warp_max(mx);
-  if (lane == 0) atomicMax(maxdeg, mx);
+  if (lane == 0 && mx) atomicMax(maxdeg, mx);
+  const uint64_t lo = V * wid / W, hi = V * (wid + 1) / W;
+  if (lo >= hi) return;
+  uint32_t a = 0, b = nn;                                           // last t with off[t] <= lo
+  while (b - a > 1) {
+    const uint32_t m = (a + b) >> 1;
+    if (off[m] <= lo) a = m; else b = m;
+  }
+  uint64_t pos = lo;
+  for (uint32_t t = a; pos < hi; ++t) {
+    const uint64_t s0 = off[t], s1 = off[t + 1];
+    if (s1 <= pos) continue;
+    const uint32_t i0 = (uint32_t)(pos - s0), i1 = (uint32_t)((s1 < hi ? s1 : hi) - s0);
+    const uint32_t *src = pool + start[t];
+    uint32_t *dst = nbr + s0;
+    for (uint32_t j0 = i0; j0 < i1; j0 += 128) {                    // 4 loads in flight per lane
+      uint32_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { const uint32_t i = j0 + u * 32 + lane; v[u] = i < i1 ? src[i] : 0u; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { const uint32_t i = j0 + u * 32 + lane; if (i < i1) dst[i] = v[u]; }
+    }
+    pos = s0 + i1;
+  }
 }
 
 __global__ void k_edge_pairs(const uint64_t *edge_off, uint32_t E, unsigned long long *T) {
@@ -414,9 +434,8 @@ extern "C" hgp_status hgp_unique_neighbors(hgp_ctx *c, const hgp_csr *g, uint32_
   out->nbr = dalloc_n<uint32_t>(c, V, &st);
   if (st) { free_nbrs(c, out); return st; }
   unsigned int *d_max = counters + 3;
-  hgp_status s = launch(c, "nbr_pack", k_nbr_pack, dim3(nn / 8 + 1 < 16u * c->sm_count ? nn / 8 + 1 : 16u * c->sm_count),
-                        dim3(256), 0, (const uint32_t *)pool, (const uint64_t *)start, (const uint32_t *)cnt,
-                        (const uint64_t *)out->off, nn, out->nbr, d_max);
+  hgp_status s = launch(c, "nbr_pack", k_seg_pack_flat, dim3(8u * c->sm_count), dim3(256), 0, (const uint32_t *)pool,
+                        (const uint64_t *)start, (const uint32_t *)cnt, (const uint64_t *)out->off, nn, V, out->nbr, d_max);
   if (s) { free_nbrs(c, out); return s; }
   uint32_t mx = 0;
   s = read_back(c, d_max, 4, &mx);

@@ -46,8 +46,24 @@ def run(hg, omega, delta, unfused):
     print(hg.name, "unfused" if unfused else "fused", "levels", len(levels), "conn", q["connectivity"], "k", k, flush=True)
 
 
+def hubs(seed=7, N=12000, big=(9000, 40), small=1000, smax=30):
+    """Edges of 9000 pins among small ones: fused-level hub nodes (b > 8192, hub.cu) and a5 coarse
+    hubs (|N(a)| + |N(b)| > 16384, the key-partitioned coarse tier)."""
+    rng = np.random.default_rng(seed)
+    sizes = list(big) + [int(x) for x in rng.integers(2, smax, size=small)]
+    pins, nsrc, off = [], [], [0]
+    for s in sizes:
+        pins.extend(rng.choice(N, size=s, replace=False).tolist())
+        nsrc.append(int(rng.integers(0, 3)) if s > 2 else 1)
+        off.append(len(pins))
+    return hgpgen.Hypergraph(N, np.array(off, dtype=np.uint64), np.array(nsrc, dtype=np.uint32),
+                             np.array(pins, dtype=np.uint32), rng.integers(1, 9, size=len(sizes)).astype(np.uint32),
+                             np.ones(N, dtype=np.uint32), name="hubs")
+
+
 if __name__ == "__main__":
     for unfused in (False, True):
+        run(hubs(), 8, 10 ** 6, unfused)
         run(hgpgen.tiny(1), 16, 32, unfused)
         run(hgpgen.snn(2, layers=3, rows=20, cols=20, fanout=30, window=7, rewire=0.1), 64, 256, unfused)
         run(hgpgen.vlsi(3, 4000, 4000, dmax=300, in_cap=64), 32, 128, unfused)
