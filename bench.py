@@ -482,8 +482,13 @@ def main():
         for x in (g2, cg2, cnb2):
             x.free()
         if not args.no_refine:
-            hier_q, refine = refine_leg(hgp, ctx, hierarchy, omega, delta, stream)
-            hier["initial_partition"] = hier_q
+            try:
+                hier_q, refine = refine_leg(hgp, ctx, hierarchy, omega, delta, stream)
+                hier["initial_partition"] = hier_q
+            except hgp.HgpError as ex:   # an optional leg: its status is reported, the line stands
+                # (e.g. C5: more than 2^29 inbound events for f4's 32-bit event keys -> HGP_E_OVERFLOW)
+                refine = {"error": str(ex)}
+                torch.cuda.synchronize()
     else:   # the sharded driver (shard.coarsen_sharded): same levels as hgp_coarsen, per-phase split
         def hierarchy_sharded():
             g = hgp.build_csr(ctx, N, dev["edge_off"], dev["edge_nsrc"], dev["pins"], dev["edge_w"], dev["node_w"])
