@@ -202,6 +202,7 @@ enum {
   HGP_TIER_FUSED_H = 19,     /* fused a2+a3, hub nodes: key-partitioned shared tables (hub.cu) */
   HGP_TIER_CNBRS_H = 20,     /* a5 coarse neighbours of hub coarse nodes, key-partitioned */
   HGP_TIER_CNBRS_A2 = 21,    /* a5 coarse neighbours, 8192-slot table (between A and M) */
+  HGP_TIER_SCORE_HUB = 22,   /* a3 on big N(n) (> 2048), key-partitioned shared tables (score_hub.cu) */
   HGP_TIERS = 24
 };
 /* HOST out[HGP_TIERS] <- the counters (synchronises); reset != 0 zeroes them afterwards. */

@@ -339,9 +339,21 @@ hgp_status launch_score_tiers(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t max_
   // neighbourhoods -> bigA, nodes needing 64-bit eta -> wide
   J.list = first_list; J.list_count = first_count;
   J.big_list = bigA; J.big_count = counts + 0; J.wide_list = wide; J.wide_count = counts + 1;
-  HGP_TRY(launch_score_flat<PIMAX>(c, J, nn, J.E));
+  const uint64_t *cv = nullptr;
+  const uint2 *wmu = nullptr;
+  HGP_TRY(launch_score_flat<PIMAX>(c, J, nn, J.E, &cv, &wmu));
+  const uint32_t *bigL = bigA, *bigC = counts + 0;
+  if (max_deg > (1u << (kSALog - 1)) && !c->opt.no_hub) {
+    // big neighbourhoods: the key-partitioned tier (score_hub.cu); what it leaves -> B as before
+    uint32_t hb = 0;
+    HGP_TRY(read_back(c, counts + 0, 4, &hb));
+    if (hb) {
+      HGP_TRY(score_hub_t<PIMAX>(c, J, cv, wmu, bigA, counts + 0, hb, lists + 3 * (size_t)nn, counts + 3));
+      bigL = lists + 3 * (size_t)nn; bigC = counts + 3;
+    }
+  }
   if (max_deg > (1u << (kSALog - 1))) {   // B: big neighbourhoods, packed (overflow -> wide)
-    J.list = bigA; J.list_count = counts + 0; J.cap = 1u << (kSBLog - 1); J.log2s = kSBLog; J.tier = HGP_TIER_SCORE_B;
+    J.list = bigL; J.list_count = bigC; J.cap = 1u << (kSBLog - 1); J.log2s = kSBLog; J.tier = HGP_TIER_SCORE_B;
     J.big_list = huge; J.big_count = counts + 2;
     HGP_TRY(launch(c, "score_B", k_score<kSBThreads, kModeP32, true, PIMAX>, dim3(c->sm_count), dim3(kSBThreads),
                    (8u << kSBLog) + 16, J));

@@ -38,7 +38,13 @@ struct ScoreJob {
 enum { kModeP32 = 0, kModeWide = 1, kModeSplit = 2 };
 
 template <int PIMAX>
-hgp_status launch_score_flat(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t E);
+hgp_status launch_score_flat(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t E, const uint64_t **cv_out = nullptr,
+                             const uint2 **wmu_out = nullptr);
+// score_hub.cu: the key-partitioned a3 tier for listed nodes with big N(n); the nodes it leaves
+// are appended to lu / lu_count
+template <int PIMAX>
+hgp_status score_hub_t(hgp_ctx *c, const ScoreJob &J, const uint64_t *cv, const uint2 *wmu, const uint32_t *list,
+                       const uint32_t *list_count, uint32_t hcount, uint32_t *lu, uint32_t *lu_count);
 
 template <int PIMAX>
 struct Top {   // best-first list of (score, id); empty entries are (0, 0): every real score >= 1

@@ -446,7 +446,8 @@ __global__ void k_edge_cv2(const uint64_t *edge_off, const uint32_t *edge_w, uin
 // First tier of a3 on an existing N(n): nodes of the list (or all of [J.lo, J.hi)) with
 // |N(n)| <= 2048; larger neighbourhoods -> big_list, nodes needing 64-bit eta -> wide_list.
 template <int PIMAX>
-hgp_status launch_score_flat(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t E) {
+hgp_status launch_score_flat(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t E, const uint64_t **cv_out,
+                             const uint2 **wmu_out) {
   static uint64_t attr_dev = 0;   // per device: cudaFuncSetAttribute applies to the current one
   if (once_per_device(&attr_dev, c->device)) {
     cudaFuncSetAttribute(k_score_flat<PIMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, flat_smem());
@@ -462,12 +463,14 @@ hgp_status launch_score_flat(hgp_ctx *c, ScoreJob J, uint32_t nn, uint32_t E) {
   HGP_TRY(launch(c, "pack_wmu", k_pack_wmu2, dim3(J.N ? (div_up(J.N, 256) < 4096 ? div_up(J.N, 256) : 4096) : 0), dim3(256),
                  0, J.node_w, J.in_mu, J.N, wmu, mx));
   J.max_in_mu = mx;
+  if (cv_out) *cv_out = cv;
+  if (wmu_out) *wmu_out = wmu;
   const uint32_t grid = J.list ? 4u * c->sm_count : (nn < 4u * c->sm_count ? (nn ? nn : 1) : 4u * c->sm_count);
   return launch(c, "score_F", k_score_flat<PIMAX>, dim3(grid), dim3(kFThreads), flat_smem(), J, (const uint64_t *)cv,
                 (const uint2 *)wmu);
 }
 
-template hgp_status launch_score_flat<4>(hgp_ctx *, ScoreJob, uint32_t, uint32_t);
-template hgp_status launch_score_flat<16>(hgp_ctx *, ScoreJob, uint32_t, uint32_t);
+template hgp_status launch_score_flat<4>(hgp_ctx *, ScoreJob, uint32_t, uint32_t, const uint64_t **, const uint2 **);
+template hgp_status launch_score_flat<16>(hgp_ctx *, ScoreJob, uint32_t, uint32_t, const uint64_t **, const uint2 **);
 
 }  // namespace hgp

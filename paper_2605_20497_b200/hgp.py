@@ -303,7 +303,7 @@ class Ctx:
 
     TIERS = ["fused_S", "fused_A", "fused_M", "fused_B", "nbrs_1", "nbrs_2", "nbrs_3", "score_nointer",
              "score_packed", "score_split", "score_B", "score_W", "score_H", "cnbrs_A", "cnbrs_M", "cnbrs_B",
-             "cnbrs_C", "jump", "fused_W", "fused_H", "cnbrs_H", "cnbrs_A2"]
+             "cnbrs_C", "jump", "fused_W", "fused_H", "cnbrs_H", "cnbrs_A2", "score_hub"]
 
     def tier_counts(self, reset: bool = False) -> dict:
         """hgp_tier_counts: nodes processed per kernel tier (include/hgp.h HGP_TIER_*)."""

@@ -77,8 +77,8 @@ def test_unfused_hub_tiers(hgp, ctx):
     and 1500 pins among many small ones."""
     ctx.tier_counts(reset=True)
     _unfused_level(hgp, ctx, _hubs(0, 30000, [17500, 7000, 3000, 1500, 40, 2]), 8, 10 ** 6)   # a5 hubs: tier H
-    with ctx.options(no_hub=1):                        # a5 hubs (bounds ~18000): the global-memory tier C
-        _unfused_level(hgp, ctx, _hubs(7, 12000, [9000, 40, 2], small=1000), 8, 10 ** 6)
+    with ctx.options(no_hub=1):   # a3 B and H, a5 C (bounds ~18000): the tiers the hub tiers replace
+        _unfused_level(hgp, ctx, _hubs(7, 12000, [9000, 3000, 40, 2], small=1000), 8, 10 ** 6)
     _record(ctx)
 
 
